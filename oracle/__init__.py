@@ -1,0 +1,172 @@
+"""CPU oracle for binary-image CCL -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package.  The
+product package ``paper_1708_08180_b200`` never imports it and shares no code
+with it.
+
+Contents
+--------
+* ``label_bfs``      -- O1, C flood fill (oracle/ccl_oracle.c), canonical labels.
+* ``label_twopass``  -- O2, C sequential two-pass min-root union-find.
+* ``brute_force``    -- O0, pure-Python transitive closure of the adjacency
+                        relation, for tiny images (<= ~64 px).
+* ``canonicalize``   -- SPEC.md:441-449: relabel any labeling so each class
+                        carries 1 + its minimum raster index (0 stays 0).
+
+Definition followed: L[p] = 0 if img[p] == 0, else
+1 + min raster index of p's 4- or 8-connected foreground component
+("give a unique ID to each connected region"; PAPER.md:137 the
+label is a global linear index; PAPER.md:209 4-connectivity; 8-connectivity
+per north_star; min-root convention SPEC.md:135, :140).
+
+Every function here is pinned in ``tests/test_oracle.py`` against things other
+than itself: SPEC/paper worked examples in ``tests/golden/``, closed forms,
+``scipy.ndimage.label`` (a library routine), exhaustive brute force on tiny
+shapes and invariants that fully determine the output.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ccl_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+_lock = threading.Lock()
+
+ERRORS = {1: "null pointer", 2: "bad dimensions", 3: "image too large",
+          4: "bad connectivity", 5: "out of host memory"}
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (plain gcc -O2)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", _SRC, "-o", tmp])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            sig = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
+            for name in ("oracle_bfs", "oracle_twopass"):
+                fn = getattr(lib, name)
+                fn.argtypes = sig
+                fn.restype = ctypes.c_int
+            lib.oracle_bfs_batched.argtypes = [ctypes.c_void_p, ctypes.c_int64] + sig[1:]
+            lib.oracle_bfs_batched.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _as_image(img) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(img))
+    if a.dtype != np.uint8:
+        a = np.ascontiguousarray((a != 0).astype(np.uint8))
+    return a
+
+
+def _call(name: str, img, connectivity: int) -> np.ndarray:
+    a = _as_image(img)
+    if a.ndim != 2:
+        raise ValueError("expected a 2D image")
+    H, W = a.shape
+    out = np.empty((H, W), dtype=np.int32)
+    rc = getattr(_load(), name)(a.ctypes.data, H, W, int(connectivity), out.ctypes.data)
+    if rc:
+        raise ValueError(f"{name}: {ERRORS.get(rc, rc)}")
+    return out
+
+
+def label_bfs(img, connectivity: int = 8) -> np.ndarray:
+    """O1: canonical labels by raster-seeded flood fill."""
+    return _call("oracle_bfs", img, connectivity)
+
+
+def label_twopass(img, connectivity: int = 8) -> np.ndarray:
+    """O2: canonical labels by sequential two-pass min-root union-find."""
+    return _call("oracle_twopass", img, connectivity)
+
+
+def label_bfs_batched(imgs, connectivity: int = 8) -> np.ndarray:
+    a = _as_image(imgs)
+    if a.ndim != 3:
+        raise ValueError("expected [B,H,W]")
+    B, H, W = a.shape
+    out = np.empty((B, H, W), dtype=np.int32)
+    rc = _load().oracle_bfs_batched(a.ctypes.data, B, H, W, int(connectivity), out.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_bfs_batched: {ERRORS.get(rc, rc)}")
+    return out
+
+
+def neighbours(y: int, x: int, H: int, W: int, connectivity: int):
+    """N4 / N8 of (x, y), clipped to the image, no wrap-around."""
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            if (dy, dx) == (0, 0) or (connectivity == 4 and dy != 0 and dx != 0):
+                continue
+            yy, xx = y + dy, x + dx
+            if 0 <= yy < H and 0 <= xx < W:
+                yield yy, xx
+
+
+def brute_force(img, connectivity: int = 8) -> np.ndarray:
+    """O0: reachability by Warshall transitive closure of the adjacency matrix
+    of foreground pixels; label = 1 + min reachable raster index.  Pure Python,
+    O(n^3): tiny images only."""
+    a = np.asarray(img)
+    H, W = a.shape
+    n = H * W
+    if n > 256:
+        raise ValueError("brute_force is for tiny images only")
+    fg = [bool(a[p // W, p % W]) for p in range(n)]
+    reach = [[i == j and fg[i] for j in range(n)] for i in range(n)]
+    for p in range(n):
+        if not fg[p]:
+            continue
+        y, x = divmod(p, W)
+        for yy, xx in neighbours(y, x, H, W, connectivity):
+            q = yy * W + xx
+            if fg[q]:
+                reach[p][q] = True
+    for k in range(n):
+        rk = reach[k]
+        for i in range(n):
+            if reach[i][k]:
+                ri = reach[i]
+                for j in range(n):
+                    if rk[j]:
+                        ri[j] = True
+    out = np.zeros((H, W), dtype=np.int32)
+    for p in range(n):
+        if fg[p]:
+            out[p // W, p % W] = 1 + min(q for q in range(n) if reach[p][q])
+    return out
+
+
+def canonicalize(labels) -> np.ndarray:
+    """map every label class to 1 + its minimum raster index;
+    label 0 (background) stays 0.  Idempotent."""
+    lab = np.asarray(labels)
+    flat = lab.reshape(-1).astype(np.int64)
+    out = np.zeros(flat.shape, dtype=np.int32)
+    fgm = flat != 0
+    if fgm.any():
+        vals = flat[fgm]
+        pos = np.nonzero(fgm)[0]
+        uniq, inv = np.unique(vals, return_inverse=True)
+        first = np.full(uniq.shape, np.iinfo(np.int64).max, dtype=np.int64)
+        np.minimum.at(first, inv, pos)
+        out[fgm] = (first[inv] + 1).astype(np.int32)
+    return out.reshape(lab.shape)
