@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the three-kernel block-parallel union-find CCL on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--conn 8]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1)
+    python bench.py --impl reference ...                  (CPU oracle arm)
+
+One step = one pass of the whole hot path (K1 local merge, K2 boundary
+analysis, K3 link) over one batch of synthetic input resident in HBM.  Rank 0
+prints ONE JSON line.  Metric: Mpixel/s for the whole job (all ranks), with
+the fraction of the HBM roofline (5 algorithmic bytes/px =
+1 B image read + 4 B label write).
+
+Timing: W untimed warm-ups; then K timed steps, each preceded (outside its
+event pair) by an L2 flush (memset of a 512 MiB buffer > 126 MB L2); CUDA
+events on the launching stream; max over ranks.  Clocks and throttle reasons
+are sampled with NVML during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Mpixel/s per GPU and whole box (fraction of HBM roofline), 1/2/4/8 B200"
+UNIT = "Mpixel/s"
+PATH_BYTES_PER_PX = 5.0          # 1 B read + 4 B write
+K1_BYTES_PER_PX = 1.0 + 1.0 / 8  # image read + bit-mask write
+K3_BYTES_PER_PX = 4.0 + 1.0 / 8  # label write + bit-mask read
+FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4"], default="C3")
+    ap.add_argument("--kind", default=None, help="C3 generator: texture|blobs|upscaled|noise|perc")
+    ap.add_argument("--conn", type=int, default=8, choices=[4, 8])
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stages", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def workload(cfg: str, kind: str | None, rank: int, world: int, conn: int):
+    """Returns (name, images uint8 [B,H,W] numpy, description dict)."""
+    import synth
+    if cfg == "C1":
+        img = synth.noise(512, 512, 0.5, seed=1 + rank)
+        return "C1 512x512 noise d=0.5", img[None], {"H": 512, "W": 512, "B": 1, "gen": "noise d=0.5"}
+    if cfg == "C2":
+        img = synth.noise(2048, 2048, 0.5, seed=105 + rank)
+        return "C2 2048x2048 noise d=0.5", img[None], {"H": 2048, "W": 2048, "B": 1, "gen": "noise d=0.5"}
+    if cfg == "C3":
+        kind = kind or "texture"
+        H = W = 8192
+        if kind == "texture":
+            img = synth.texture(H, W, seed=3001 + rank, density=0.5)
+        elif kind == "blobs":
+            img = synth.blobs(H, W, seed=3002 + rank)
+        elif kind == "upscaled":
+            img = synth.upscaled(H, W, seed=3003 + rank)
+        elif kind == "noise":
+            img = synth.noise(H, W, 0.5, seed=3004 + rank)
+        elif kind == "perc":
+            img = synth.noise(H, W, synth.percolation_density(conn), seed=3005 + rank)
+        else:
+            raise SystemExit(f"unknown --kind {kind}")
+        return f"C3 8192x8192 {kind}", img[None], {"H": H, "W": W, "B": 1, "gen": kind}
+    if cfg == "C4":
+        B_total, H, W = 1024, 1080, 1920
+        B = B_total // world
+        distinct = min(B, 32)
+        base = synth.frames(distinct, H, W, first=rank * B)
+        imgs = np.concatenate([base] * ((B + distinct - 1) // distinct))[:B]
+        return (f"C4 {B_total} frames 1080x1920 (DP, {B}/rank)", imgs,
+                {"H": H, "W": W, "B": B, "gen": f"texture frames, {distinct} distinct per rank, tiled"})
+    raise SystemExit(cfg)
+
+
+# ------------------------------------------------------------------- helpers
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons in a thread."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------- cpu baseline
+def cpu_oracle_rate(imgs, conn, seconds):
+    """Oracle (as it stands, single-threaded C BFS) on whole images of the
+    workload until ~`seconds` of CPU work; returns (Mpx/s, images, labels0)."""
+    import oracle
+    done_px, n, t0, first = 0, 0, time.perf_counter(), None
+    while True:
+        img = imgs[n % len(imgs)]
+        lab = oracle.label_bfs(img, conn)
+        if first is None:
+            first = lab
+        done_px += img.size
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 4 * len(imgs) and el > 1.0:
+            break
+    return done_px / el / 1e6, n, first
+
+
+# --------------------------------------------------------------------- main
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    name, imgs, desc = workload(args.config, args.kind, 0, 1, args.conn)
+    import oracle
+    # each step: a bounded sample of the workload (one image / frame)
+    sample = imgs[: max(1, min(len(imgs), 2))]
+    for _ in range(args.warmup):
+        oracle.label_bfs(sample[0], args.conn)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        for img in sample:
+            oracle.label_bfs(img, args.conn)
+        times.append(time.perf_counter() - t0)
+    px = sample[0].size * len(sample)
+    ms = 1e3 * statistics.mean(times)
+    value = px / (ms / 1e3) / 1e6
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": name, "connectivity": args.conn, **desc},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{len(sample)} image(s) of {desc['H']}x{desc['W']} per step, C BFS, 1 thread"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_1708_08180_b200 as ccl
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    name, imgs_np, desc = workload(args.config, args.kind, rank, world, args.conn)
+    B, H, W = imgs_np.shape
+    conn = args.conn
+    img = torch.from_numpy(imgs_np).to(dev)
+    out = torch.empty((B, H, W), dtype=torch.int32, device=dev)
+    ws = ccl.Workspace(B, H, W, conn, device=dev)
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    nh, nv = ccl.boundary_work_items(B, H, W)
+    launches_per_step = 2 + (1 if nh + nv > 0 else 0)
+
+    def step():
+        ccl.label(img, conn, out=out, workspace=ws)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for i in range(K):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        wall = time.perf_counter() - t0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = statistics.mean(step_ms)
+    ms = allreduce_max(ms_local, world)
+    px_rank = B * H * W
+    px_total = px_rank * world
+    value = px_total / (ms / 1e3) / 1e6
+
+    # per-kernel device times (same kernels through the per-stage C ABI)
+    kern = {}
+    if not args.no_stages:
+        k1, k2, k3 = ccl.stage_fns()
+        ks = [k1, k2, k3]
+        rec = [[] for _ in ks]
+        for i in range(max(3, min(K, 50))):
+            flush.zero_()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            for j, f in enumerate(ks):
+                f(img, conn, out, ws)
+                e[j + 1].record(stream)
+            torch.cuda.synchronize()
+            for j in range(3):
+                rec[j].append(e[j].elapsed_time(e[j + 1]))
+        for j, nm in enumerate(("k1_local_merge", "k2_boundary", "k3_link")):
+            kern[nm] = allreduce_max(statistics.mean(rec[j]), world)
+
+    peak, peak_src = load_peak()
+    path_gbs = PATH_BYTES_PER_PX * px_rank / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": name, "connectivity": conn, "B": B, "H": H, "W": W, "gen": desc["gen"],
+                   "px_per_rank": px_rank, "parallelism": f"dp{world} (independent images, no collective)",
+                   "l2": f"flushed: {args.flush_mb} MiB memset before every timed step (outside events)",
+                   "tile": "1024x16"},
+        "per_gpu_mpx_s": round(px_rank / (ms / 1e3) / 1e6, 2),
+        "wall_ms_per_step_incl_flush": round(1e3 * wall / K, 4),
+        "step_ms": {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),
+                    "max": round(max(step_ms), 5)},
+        "gpu_launches": launches_per_step * K,
+        "path_roofline": {"bytes_per_px": PATH_BYTES_PER_PX, "achieved": round(path_gbs, 1),
+                          "peak": peak, "unit": "GB/s", "frac": round(path_gbs / peak, 4)},
+    }
+    if kern:
+        line["kernels_ms"] = {k: round(v, 5) for k, v in kern.items()}
+        dom = max(kern, key=kern.get)
+        bpp = {"k1_local_merge": K1_BYTES_PER_PX, "k3_link": K3_BYTES_PER_PX}.get(dom)
+        if bpp is not None:
+            ach = bpp * px_rank / (kern[dom] / 1e3) / 1e9
+            line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                                "bytes_per_px": bpp, "peak_source": peak_src,
+                                "share_of_step": round(kern[dom] / sum(kern.values()), 3)}
+        else:
+            line["roofline"] = {"kernel": dom, "bound": "latency", "achieved": None, "peak": peak,
+                                "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src}
+    line["clocks"] = clk.summary()
+
+    # end-to-end through the C ABI with host buffers (pinned), copies timed
+    if not args.no_e2e:
+        sess = ccl.HostSession(B, H, W, conn)
+        sess.h_image.copy_(torch.from_numpy(imgs_np))
+        for _ in range(2):
+            sess.run()
+        barrier(world)
+        n_e2e = max(3, min(K, 20))
+        e2e_ms = []
+        for _ in range(n_e2e):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sess.run(stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+        e_ms = allreduce_max(statistics.mean(e2e_ms), world)
+        line["e2e"] = {"value": round(px_total / (e_ms / 1e3) / 1e6, 2), "unit": UNIT,
+                       "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes,
+                       "ms_per_step": round(e_ms, 4), "steps": n_e2e,
+                       "api": "ccl_label_host_async (pinned host buffers)"}
+        lab_gpu = sess.h_labels.numpy()
+        del sess
+    else:
+        lab_gpu = out.cpu().numpy()
+
+    # CPU oracle baseline (rank 0, N = 1 only) + parity of this run's output
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, n_imgs, lab0 = cpu_oracle_rate(imgs_np, conn, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": round(rate, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"{n_imgs} image(s) of {H}x{W} from the workload, C BFS, 1 thread"}
+        line["parity_vs_oracle"] = bool(np.array_equal(lab_gpu[0], lab0))
+    else:
+        line["cpu_baseline"] = None
+    line["gpu_launches_note"] = f"{launches_per_step} kernels/step (K1, K2, K3) in the timed loop"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * ccl.h -- C ABI of the B200 (sm_100a) connected-components-labeling library
+ * (libccl.so), the data-parallel hot path of arxiv 1708.08180:
+ *   "an optimized union-find (UF) algorithm that can label the connected
+ *    components on a 2D image ... three phases: UF-based local merge, boundary
+ *    analysis, and link"                              (abstract)
+ *
+ * Problem statement (what every entry point computes):
+ *   CCL "give[s] a unique ID to each connected region in a 2D ... grid"
+ *   (PAPER.md:24).  Input "Image I of size N x M" -- here H rows
+ *   (the paper's M) by W columns (the paper's N = imgWidth), row-major, raster
+ *   index idx(x,y) = y*W + x.  A pixel is foreground iff its
+ *   byte is nonzero (reading R1).  Neighbourhood: 4-connectivity
+ *    or 8-connectivity (north_star), clipped at the image border.
+ *   Output label of pixel p: 0 if background, else 1 + the minimum raster index
+ *   of p's component (the unique canonical form; reading R3).
+ *
+ * Conventions shared by every entry point
+ *   - Layout: contiguous row-major, row stride W, no pitch.  Batched: image b
+ *     starts at byte offset b*H*W of `images`; its labels at element offset
+ *     b*H*W of `labels_out`.  Labels are per image.
+ *   - Memory: every pointer named d_* / images / labels_out / workspace is a
+ *     CUDA device pointer on the current device; h_* pointers are host memory
+ *     (page-locked for full copy bandwidth).  The CALLER owns all memory; the
+ *     library keeps no state besides cached device attributes.
+ *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  *_async calls only enqueue work; they return before the
+ *     GPU finishes.  Device faults surface at the caller's next synchronisation.
+ *   - Errors: argument errors are detected on the host BEFORE anything is
+ *     enqueued and reported as a status code; nothing is written.  A failed
+ *     launch returns CCL_ERR_CUDA and ccl_last_cuda_error() gives the
+ *     cudaError_t.  No exceptions or aborts cross the ABI.
+ *   - Sizes: H >= 1, W >= 1, B >= 0 (B == 0 is a no-op returning CCL_OK);
+ *     H*W must be <= 2^31-1 (labels are int32), else CCL_ERR_TOO_LARGE.
+ *   - Determinism: output is bit-identical across runs, streams, tile
+ *     configurations and GPU counts (the canonical form is unique).
+ *   - Thread safety: reentrant; distinct streams may run concurrently.
+ */
+#ifndef CCL_B200_H
+#define CCL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CCL_OK = 0,
+    CCL_ERR_NULL = 1,          /* a required pointer is NULL                         */
+    CCL_ERR_DIMS = 2,          /* H < 1, W < 1, B < 0, or bad strip geometry         */
+    CCL_ERR_TOO_LARGE = 3,     /* H*W > 2^31-1 (labels would overflow int32)         */
+    CCL_ERR_CONNECTIVITY = 4,  /* connectivity not in {4, 8}                         */
+    CCL_ERR_ALIAS = 5,         /* input and output / workspace byte ranges overlap   */
+    CCL_ERR_WORKSPACE = 6,     /* workspace smaller than ccl_workspace_bytes()       */
+    CCL_ERR_CUDA = 7,          /* a CUDA runtime call or launch failed               */
+    CCL_ERR_CONFIG = 8         /* unsupported tile configuration                     */
+} ccl_status_t;
+
+/* Human-readable text for a status code (static storage, never NULL). */
+const char* ccl_status_string(ccl_status_t status);
+
+/* cudaError_t of the most recent CCL_ERR_CUDA returned on the calling thread. */
+int ccl_last_cuda_error(void);
+
+/* Device workspace (bytes) needed by the *_async entry points for B images of
+ * H x W: the global union-find parent array of the boundary analysis (one int32
+ * per pixel, only tile-edge entries are ever touched) plus the bit-packed
+ * foreground mask (one bit per pixel, rows padded to 32 px).  Returns 0 for
+ * invalid arguments. */
+size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
+
+/* Label one H x W image (device pointers).  Allocates its workspace stream-
+ * ordered (cudaMallocAsync) on the legacy default stream and frees it there;
+ * asynchronous to the host like every other launch on that stream. */
+ccl_status_t ccl_label(const uint8_t* image, int64_t H, int64_t W, int connectivity,
+                       int32_t* labels_out);
+
+/* Label B independent H x W images (device pointers), labels per image.  Same
+ * workspace policy as ccl_label. */
+ccl_status_t ccl_label_batched(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                               int connectivity, int32_t* labels_out);
+
+/* The hot path: the paper's three kernels enqueued on `stream`
+ *   K1 local merge with coarse labeling   (Alg. 1; §2.1)
+ *   K2 boundary analysis                  (Alg. 2; §2.2)
+ *   K3 final link                         (§2.3)
+ * using the caller's workspace (>= ccl_workspace_bytes(B,H,W,connectivity)
+ * bytes, 256-byte aligned, contents need not be initialised).  `images` must
+ * not overlap `labels_out` or `workspace`. */
+ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                     int connectivity, int32_t* labels_out,
+                                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* As ccl_label_batched_async with an explicit tile height (rows per K1 thread
+ * block: 8, 16 or 32; 0 = library default).  The tile width is fixed at 1024
+ * pixels (32 lanes x 32 px).  Output is identical for every tile config
+ * ("config independence"); unsupported values -> CCL_ERR_CONFIG. */
+ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                         int connectivity, int32_t* labels_out,
+                                         void* workspace, size_t workspace_bytes,
+                                         int tile_rows, void* stream);
+
+/* The three stages individually (same arguments as ccl_label_batched_cfg_async),
+ * for per-kernel timing and stage tests.  They must be enqueued in this order on
+ * one stream with the same workspace:
+ *   ccl_stage_local_merge  K1: reads images; writes the bit-packed mask and the
+ *                          tile-edge entries of the parent array (workspace).
+ *   ccl_stage_boundary     K2: unions every foreground edge that crosses a tile
+ *                          boundary into the parent array (workspace only).
+ *   ccl_stage_link         K3: writes labels_out for every pixel.          */
+ccl_status_t ccl_stage_local_merge(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                   int connectivity, void* workspace, size_t workspace_bytes,
+                                   int tile_rows, void* stream);
+ccl_status_t ccl_stage_boundary(int64_t B, int64_t H, int64_t W, int connectivity,
+                                void* workspace, size_t workspace_bytes, int tile_rows,
+                                void* stream);
+ccl_status_t ccl_stage_link(int64_t B, int64_t H, int64_t W, int connectivity,
+                            int32_t* labels_out, void* workspace, size_t workspace_bytes,
+                            int tile_rows, void* stream);
+
+/* Number of K2 boundary work items for the given geometry and tile height:
+ * horizontal tile-edge segments (one warp each) and vertical tile-edge pixels
+ * (one thread each).  Host-only bookkeeping (cf. Eq. (1)-(2), PAPER.md:326-334,
+ * which counts boundary cells for the paper's {32,16} blocks).  Returns -1 on
+ * invalid arguments. */
+int64_t ccl_boundary_work_items(int64_t B, int64_t H, int64_t W, int tile_rows,
+                                int64_t* horizontal_segments, int64_t* vertical_pixels);
+
+/* End-to-end entry (host buffers): copies h_images (B*H*W bytes) to the device,
+ * runs the three kernels and copies the labels back into h_labels (B*H*W int32),
+ * all enqueued on `stream` in row-band chunks so copies overlap compute.
+ * d_scratch is caller-owned device memory of >= ccl_host_scratch_bytes() bytes.
+ * Returns after enqueueing; the caller synchronises `stream` before reading
+ * h_labels.  h_images/h_labels should be page-locked (cudaHostAlloc /
+ * cudaHostRegister) for asynchronous copies. */
+size_t ccl_host_scratch_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
+ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H, int64_t W,
+                                  int connectivity, int32_t* h_labels,
+                                  void* d_scratch, size_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CCL_B200_H */

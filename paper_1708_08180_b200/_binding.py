@@ -1,0 +1,218 @@
+"""Thin ctypes binding over libccl.so (include/ccl.h).  Argument marshalling
+only: every step of the labeling runs in the library's CUDA kernels.  PyTorch
+supplies device memory (caching allocator) and the current CUDA stream.
+
+There is deliberately no fallback: if libccl.so is missing or cannot be
+loaded, importing this module raises (build it with
+``python -m paper_1708_08180_b200._build`` or ``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libccl.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1708_08180_b200._build` "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+_i64, _int, _sz, _vp = ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p
+
+# name -> (restype, argtypes); mirrors include/ccl.h
+SIGNATURES = {
+    "ccl_status_string": (ctypes.c_char_p, [_int]),
+    "ccl_last_cuda_error": (_int, []),
+    "ccl_workspace_bytes": (_sz, [_i64, _i64, _i64, _int]),
+    "ccl_label": (_int, [_vp, _i64, _i64, _int, _vp]),
+    "ccl_label_batched": (_int, [_vp, _i64, _i64, _i64, _int, _vp]),
+    "ccl_label_batched_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
+    "ccl_label_batched_cfg_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _int, _vp]),
+    "ccl_stage_local_merge": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _sz, _int, _vp]),
+    "ccl_stage_boundary": (_int, [_i64, _i64, _i64, _int, _vp, _sz, _int, _vp]),
+    "ccl_stage_link": (_int, [_i64, _i64, _i64, _int, _vp, _vp, _sz, _int, _vp]),
+    "ccl_boundary_work_items": (_i64, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "ccl_host_scratch_bytes": (_sz, [_i64, _i64, _i64, _int]),
+    "ccl_label_host_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+STATUS = {0: "CCL_OK", 1: "CCL_ERR_NULL", 2: "CCL_ERR_DIMS", 3: "CCL_ERR_TOO_LARGE",
+          4: "CCL_ERR_CONNECTIVITY", 5: "CCL_ERR_ALIAS", 6: "CCL_ERR_WORKSPACE",
+          7: "CCL_ERR_CUDA", 8: "CCL_ERR_CONFIG"}
+
+
+class CCLError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        msg = _lib.ccl_status_string(status).decode()
+        if status == 7:
+            msg += f" (cudaError {_lib.ccl_last_cuda_error()})"
+        super().__init__(f"{where}: {self.name}: {msg}")
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        raise CCLError(status, where)
+
+
+def raw():
+    """The underlying ctypes CDLL (tests call the C ABI through it)."""
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return _lib.ccl_status_string(status).decode()
+
+
+def workspace_bytes(B: int, H: int, W: int, connectivity: int = 8) -> int:
+    return int(_lib.ccl_workspace_bytes(B, H, W, connectivity))
+
+
+def boundary_work_items(B: int, H: int, W: int, tile_rows: int = 0):
+    h, v = _i64(0), _i64(0)
+    total = _lib.ccl_boundary_work_items(B, H, W, tile_rows, ctypes.byref(h), ctypes.byref(v))
+    if total < 0:
+        raise ValueError("invalid geometry")
+    return int(h.value), int(v.value)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _shape3(t):
+    if t.dim() == 2:
+        return 1, int(t.shape[0]), int(t.shape[1])
+    if t.dim() == 3:
+        return int(t.shape[0]), int(t.shape[1]), int(t.shape[2])
+    raise ValueError(f"expected [H,W] or [B,H,W], got shape {tuple(t.shape)}")
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_image(image):
+    torch = _torch()
+    if not isinstance(image, torch.Tensor) or not image.is_cuda:
+        raise TypeError("image must be a CUDA tensor (there is no CPU path)")
+    if image.dtype != torch.uint8:
+        raise TypeError(f"image must be uint8, got {image.dtype}")
+    if not image.is_contiguous():
+        raise ValueError("image must be contiguous (row-major, no pitch)")
+
+
+class Workspace:
+    """Reusable device workspace (a torch uint8 buffer) for repeated calls."""
+
+    def __init__(self, B: int, H: int, W: int, connectivity: int = 8, device=None):
+        torch = _torch()
+        n = workspace_bytes(B, H, W, connectivity)
+        if n == 0:
+            raise ValueError("invalid geometry")
+        self.nbytes = n
+        self.buf = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+
+    def ptr(self):
+        return ctypes.c_void_p(self.buf.data_ptr())
+
+
+def label(image, connectivity: int = 8, *, out=None, workspace: Workspace | None = None,
+          tile_rows: int = 0, stream=None):
+    """Label a uint8 CUDA image [H,W] or batch [B,H,W]; returns int32 labels of
+    the same shape (0 = background, 1 + min raster index per component, per
+    image).  Enqueued on ``stream`` (default: torch's current stream)."""
+    torch = _torch()
+    _check_image(image)
+    B, H, W = _shape3(image)
+    if out is None:
+        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+    elif out.dtype != torch.int32 or out.shape != image.shape or not out.is_contiguous():
+        raise ValueError("out must be a contiguous int32 tensor of the image's shape")
+    if B == 0:
+        return out
+    if workspace is None:
+        workspace = Workspace(B, H, W, connectivity, device=image.device)
+    _check(_lib.ccl_label_batched_cfg_async(
+        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+        workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(stream)), "ccl_label_batched_cfg_async")
+    return out
+
+
+def stages(image, connectivity: int, out, workspace: Workspace, tile_rows: int = 0, stream=None):
+    """Enqueue K1, K2, K3 as three separate C-ABI calls (per-kernel timing)."""
+    B, H, W = _shape3(image)
+    s = _stream_ptr(stream)
+    ws = workspace.ptr()
+    _check(_lib.ccl_stage_local_merge(ctypes.c_void_p(image.data_ptr()), B, H, W, connectivity, ws,
+                                      workspace.nbytes, tile_rows, s), "ccl_stage_local_merge")
+    _check(_lib.ccl_stage_boundary(B, H, W, connectivity, ws, workspace.nbytes, tile_rows, s),
+           "ccl_stage_boundary")
+    _check(_lib.ccl_stage_link(B, H, W, connectivity, ctypes.c_void_p(out.data_ptr()), ws,
+                               workspace.nbytes, tile_rows, s), "ccl_stage_link")
+
+
+def stage_fns():
+    """(k1, k2, k3) callables taking (image, connectivity, out, workspace,
+    tile_rows, stream) for per-kernel event timing."""
+    def k1(image, conn, out, ws, tile_rows=0, stream=None):
+        B, H, W = _shape3(image)
+        _check(_lib.ccl_stage_local_merge(ctypes.c_void_p(image.data_ptr()), B, H, W, conn, ws.ptr(),
+                                          ws.nbytes, tile_rows, _stream_ptr(stream)), "k1")
+
+    def k2(image, conn, out, ws, tile_rows=0, stream=None):
+        B, H, W = _shape3(image)
+        _check(_lib.ccl_stage_boundary(B, H, W, conn, ws.ptr(), ws.nbytes, tile_rows,
+                                       _stream_ptr(stream)), "k2")
+
+    def k3(image, conn, out, ws, tile_rows=0, stream=None):
+        B, H, W = _shape3(image)
+        _check(_lib.ccl_stage_link(B, H, W, conn, ctypes.c_void_p(out.data_ptr()), ws.ptr(),
+                                   ws.nbytes, tile_rows, _stream_ptr(stream)), "k3")
+    return k1, k2, k3
+
+
+class HostSession:
+    """End-to-end use from host memory: pinned host buffers + device scratch;
+    ``run()`` enqueues H2D copy, the three kernels and the D2H copy through the
+    C ABI (ccl_label_host_async) and synchronises."""
+
+    def __init__(self, B: int, H: int, W: int, connectivity: int = 8):
+        torch = _torch()
+        self.B, self.H, self.W, self.conn = B, H, W, connectivity
+        n = int(_lib.ccl_host_scratch_bytes(B, H, W, connectivity))
+        if n == 0:
+            raise ValueError("invalid geometry")
+        self.scratch_bytes = n
+        self.scratch = torch.empty(n, dtype=torch.uint8, device="cuda")
+        self.h_image = torch.empty((B, H, W), dtype=torch.uint8, pin_memory=True)
+        self.h_labels = torch.empty((B, H, W), dtype=torch.int32, pin_memory=True)
+
+    def run(self, stream=None):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _check(_lib.ccl_label_host_async(
+            ctypes.c_void_p(self.h_image.data_ptr()), self.B, self.H, self.W, self.conn,
+            ctypes.c_void_p(self.h_labels.data_ptr()), ctypes.c_void_p(self.scratch.data_ptr()),
+            self.scratch_bytes, ctypes.c_void_p(s.cuda_stream)), "ccl_label_host_async")
+        s.synchronize()
+        return self.h_labels
+
+    @property
+    def h2d_bytes(self):
+        return self.B * self.H * self.W
+
+    @property
+    def d2h_bytes(self):
+        return 4 * self.B * self.H * self.W

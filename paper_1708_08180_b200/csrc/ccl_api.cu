@@ -1,0 +1,312 @@
+// ccl_api.cu -- host side of libccl.so: argument validation, launch geometry,
+// workspace layout and the C ABI declared in include/ccl.h.
+#include "../../include/ccl.h"
+#include "ccl_kernels.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+constexpr int kDefaultTileRows = 16;
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Plan {
+    ccl::Geom g;
+    int ty;
+    size_t G_bytes, bits_bytes;
+};
+
+ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
+    if (B < 0 || H < 1 || W < 1) return CCL_ERR_DIMS;
+    if (H > INT32_MAX / W) return CCL_ERR_TOO_LARGE;
+    if (conn != 4 && conn != 8) return CCL_ERR_CONNECTIVITY;
+    return CCL_OK;
+}
+
+ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows, Plan& p) {
+    ccl_status_t st = check_geometry(B, H, W, conn);
+    if (st != CCL_OK) return st;
+    if (tile_rows == 0) tile_rows = kDefaultTileRows;
+    if (tile_rows != 8 && tile_rows != 16 && tile_rows != 32) return CCL_ERR_CONFIG;
+    if (B > INT32_MAX) return CCL_ERR_DIMS;
+    p.ty = tile_rows;
+    p.g.B = int(B);
+    p.g.H = int(H);
+    p.g.W = int(W);
+    p.g.WW = int((W + 31) / 32);
+    p.g.tiles_x = int((W + ccl::kTileW - 1) / ccl::kTileW);
+    p.g.tiles_y = int((H + tile_rows - 1) / tile_rows);
+    p.g.npx = H * W;
+    p.g.nwords = H * int64_t(p.g.WW);
+    p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
+    p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
+    return CCL_OK;
+}
+
+ccl_status_t cuda_fail(cudaError_t e) {
+    g_last_cuda_error = int(e);
+    return CCL_ERR_CUDA;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return na && nb && pa < pb + nb && pb < pa + na;
+}
+
+template <int TY>
+size_t smem_bytes() { return sizeof(ccl::TileSmem<TY>); }
+
+template <int TY, int CONN, bool VEC>
+cudaError_t setup_attrs() {
+    // opt in to > 48 KB dynamic shared memory once per instantiation
+    static cudaError_t once = [] {
+        cudaError_t e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem_bytes<TY>()));
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem_bytes<TY>()));
+    }();
+    return once;
+}
+
+enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7 };
+
+template <int TY, int CONN, bool VEC>
+cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* out, void* ws,
+                       cudaStream_t s) {
+    cudaError_t e = setup_attrs<TY, CONN, VEC>();
+    if (e != cudaSuccess) return e;
+    const ccl::Geom& g = p.g;
+    int32_t* G = static_cast<int32_t*>(ws);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes);
+    const long long ntiles = (long long)g.B * g.tiles_x * g.tiles_y;
+    if (ntiles == 0) return cudaSuccess;
+    const size_t smem = smem_bytes<TY>();
+    if (stages & kK1) {
+        ccl::k_local_merge<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(img, g, bits, G);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (stages & kK2) {
+        const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
+        const long long n_v = (long long)g.B * g.H * (g.tiles_x - 1);
+        const long long blocks_h = (n_h + 7) / 8, blocks_v = (n_v + 255) / 256;
+        if (blocks_h + blocks_v > 0) {
+            ccl::k_boundary<TY, CONN><<<unsigned(blocks_h + blocks_v), 256, 0, s>>>(g, bits, G, n_h,
+                                                                                   blocks_h);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    if (stages & kK3) {
+        ccl::k_link<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(g, bits, G, out);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+template <int TY>
+cudaError_t dispatch_conn(const Plan& p, int conn, bool vec, int stages, const uint8_t* img,
+                          int32_t* out, void* ws, cudaStream_t s) {
+    if (conn == 4)
+        return vec ? run_stages<TY, 4, true>(p, stages, img, out, ws, s)
+                   : run_stages<TY, 4, false>(p, stages, img, out, ws, s);
+    return vec ? run_stages<TY, 8, true>(p, stages, img, out, ws, s)
+               : run_stages<TY, 8, false>(p, stages, img, out, ws, s);
+}
+
+// The 128-bit paths need 16-byte aligned rows: W % 16 == 0 for the uint8 image
+// (which also gives W % 4 == 0 for the int32 labels) and aligned base pointers.
+bool vector_ok(const Plan& p, const void* img, const void* out) {
+    if (p.g.W % 16) return false;
+    if (img && (reinterpret_cast<uintptr_t>(img) & 15)) return false;
+    if (out && (reinterpret_cast<uintptr_t>(out) & 15)) return false;
+    return true;
+}
+
+ccl_status_t run(const Plan& p, int conn, int stages, const uint8_t* img, int32_t* out, void* ws,
+                 cudaStream_t s) {
+    const bool vec = vector_ok(p, img, out);
+    cudaError_t e;
+    switch (p.ty) {
+        case 8: e = dispatch_conn<8>(p, conn, vec, stages, img, out, ws, s); break;
+        case 16: e = dispatch_conn<16>(p, conn, vec, stages, img, out, ws, s); break;
+        case 32: e = dispatch_conn<32>(p, conn, vec, stages, img, out, ws, s); break;
+        default: return CCL_ERR_CONFIG;
+    }
+    return e == cudaSuccess ? CCL_OK : cuda_fail(e);
+}
+
+ccl_status_t validate_buffers(const Plan& p, const uint8_t* img, const int32_t* out, void* ws,
+                              size_t ws_bytes, int stages) {
+    const size_t n = size_t(p.g.B) * size_t(p.g.npx);
+    if (n == 0) return CCL_OK;
+    if ((stages & kK1) && !img) return CCL_ERR_NULL;
+    if ((stages & kK3) && !out) return CCL_ERR_NULL;
+    if (!ws) return CCL_ERR_NULL;
+    if (ws_bytes < p.G_bytes + p.bits_bytes) return CCL_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(ws) % 4) return CCL_ERR_WORKSPACE;
+    if (img && out && overlaps(img, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
+    if (img && overlaps(img, n, ws, ws_bytes)) return CCL_ERR_ALIAS;
+    if (out && overlaps(out, n * sizeof(int32_t), ws, ws_bytes)) return CCL_ERR_ALIAS;
+    return CCL_OK;
+}
+
+ccl_status_t label_alloc(const uint8_t* images, int64_t B, int64_t H, int64_t W, int conn,
+                         int32_t* out) {
+    Plan p;
+    ccl_status_t st = make_plan(B, H, W, conn, 0, p);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    if (!images || !out) return CCL_ERR_NULL;
+    const size_t n = size_t(B) * size_t(p.g.npx);
+    if (overlaps(images, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
+    void* ws = nullptr;
+    const size_t bytes = p.G_bytes + p.bits_bytes;
+    cudaError_t e = cudaMallocAsync(&ws, bytes, 0);
+    if (e != cudaSuccess) return cuda_fail(e);
+    st = run(p, conn, kAll, images, out, ws, 0);
+    e = cudaFreeAsync(ws, 0);
+    if (st == CCL_OK && e != cudaSuccess) return cuda_fail(e);
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ccl_status_string(ccl_status_t status) {
+    switch (status) {
+        case CCL_OK: return "ok";
+        case CCL_ERR_NULL: return "a required pointer is NULL";
+        case CCL_ERR_DIMS: return "invalid dimensions (need H >= 1, W >= 1, B >= 0)";
+        case CCL_ERR_TOO_LARGE: return "image too large: H*W must be <= 2^31-1";
+        case CCL_ERR_CONNECTIVITY: return "connectivity must be 4 or 8";
+        case CCL_ERR_ALIAS: return "input and output/workspace buffers overlap";
+        case CCL_ERR_WORKSPACE: return "workspace too small or misaligned";
+        case CCL_ERR_CUDA: return "CUDA error (see ccl_last_cuda_error)";
+        case CCL_ERR_CONFIG: return "unsupported tile configuration";
+    }
+    return "unknown status";
+}
+
+int ccl_last_cuda_error(void) { return g_last_cuda_error; }
+
+size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity) {
+    Plan p;
+    if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
+    return p.G_bytes + p.bits_bytes;
+}
+
+ccl_status_t ccl_label(const uint8_t* image, int64_t H, int64_t W, int connectivity,
+                       int32_t* labels_out) {
+    return label_alloc(image, 1, H, W, connectivity, labels_out);
+}
+
+ccl_status_t ccl_label_batched(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                               int connectivity, int32_t* labels_out) {
+    return label_alloc(images, B, H, W, connectivity, labels_out);
+}
+
+ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                         int connectivity, int32_t* labels_out, void* workspace,
+                                         size_t workspace_bytes, int tile_rows, void* stream) {
+    Plan p;
+    ccl_status_t st = make_plan(B, H, W, connectivity, tile_rows, p);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    st = validate_buffers(p, images, labels_out, workspace, workspace_bytes, kAll);
+    if (st != CCL_OK) return st;
+    return run(p, connectivity, kAll, images, labels_out, workspace, static_cast<cudaStream_t>(stream));
+}
+
+ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                     int connectivity, int32_t* labels_out, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    return ccl_label_batched_cfg_async(images, B, H, W, connectivity, labels_out, workspace,
+                                       workspace_bytes, 0, stream);
+}
+
+static ccl_status_t stage(const uint8_t* images, int64_t B, int64_t H, int64_t W, int conn,
+                          int32_t* out, void* ws, size_t ws_bytes, int tile_rows, int which,
+                          void* stream) {
+    Plan p;
+    ccl_status_t st = make_plan(B, H, W, conn, tile_rows, p);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    st = validate_buffers(p, images, out, ws, ws_bytes, which);
+    if (st != CCL_OK) return st;
+    // the vector decision must match across stages: K1 decides on the image,
+    // K3 on the output; both reduce to W % 16 == 0 for aligned buffers
+    return run(p, conn, which, images, out, ws, static_cast<cudaStream_t>(stream));
+}
+
+ccl_status_t ccl_stage_local_merge(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                   int connectivity, void* workspace, size_t workspace_bytes,
+                                   int tile_rows, void* stream) {
+    return stage(images, B, H, W, connectivity, nullptr, workspace, workspace_bytes, tile_rows, kK1,
+                 stream);
+}
+
+ccl_status_t ccl_stage_boundary(int64_t B, int64_t H, int64_t W, int connectivity, void* workspace,
+                                size_t workspace_bytes, int tile_rows, void* stream) {
+    return stage(nullptr, B, H, W, connectivity, nullptr, workspace, workspace_bytes, tile_rows, kK2,
+                 stream);
+}
+
+ccl_status_t ccl_stage_link(int64_t B, int64_t H, int64_t W, int connectivity, int32_t* labels_out,
+                            void* workspace, size_t workspace_bytes, int tile_rows, void* stream) {
+    return stage(nullptr, B, H, W, connectivity, labels_out, workspace, workspace_bytes, tile_rows,
+                 kK3, stream);
+}
+
+int64_t ccl_boundary_work_items(int64_t B, int64_t H, int64_t W, int tile_rows,
+                                int64_t* horizontal_segments, int64_t* vertical_pixels) {
+    Plan p;
+    if (make_plan(B, H, W, 4, tile_rows, p) != CCL_OK) return -1;
+    const int64_t nh = B * int64_t(p.g.tiles_y - 1) * p.g.tiles_x;
+    const int64_t nv = B * H * int64_t(p.g.tiles_x - 1);
+    if (horizontal_segments) *horizontal_segments = nh;
+    if (vertical_pixels) *vertical_pixels = nv;
+    return nh + nv;
+}
+
+size_t ccl_host_scratch_bytes(int64_t B, int64_t H, int64_t W, int connectivity) {
+    Plan p;
+    if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
+    const size_t n = size_t(B) * size_t(p.g.npx);
+    return align_up(n) + align_up(n * sizeof(int32_t)) + p.G_bytes + p.bits_bytes;
+}
+
+ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H, int64_t W,
+                                  int connectivity, int32_t* h_labels, void* d_scratch,
+                                  size_t scratch_bytes, void* stream) {
+    Plan p;
+    ccl_status_t st = make_plan(B, H, W, connectivity, 0, p);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    if (!h_images || !h_labels || !d_scratch) return CCL_ERR_NULL;
+    if (scratch_bytes < ccl_host_scratch_bytes(B, H, W, connectivity)) return CCL_ERR_WORKSPACE;
+    const size_t n = size_t(B) * size_t(p.g.npx);
+    if (overlaps(h_images, n, h_labels, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* base = static_cast<char*>(d_scratch);
+    uint8_t* d_img = reinterpret_cast<uint8_t*>(base);
+    int32_t* d_out = reinterpret_cast<int32_t*>(base + align_up(n));
+    void* ws = base + align_up(n) + align_up(n * sizeof(int32_t));
+    cudaError_t e = cudaMemcpyAsync(d_img, h_images, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    st = run(p, connectivity, kAll, d_img, d_out, ws, s);
+    if (st != CCL_OK) return st;
+    e = cudaMemcpyAsync(h_labels, d_out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return CCL_OK;
+}
+
+}  // extern "C"

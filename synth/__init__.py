@@ -69,16 +69,19 @@ _DEFAULT_OCTAVES = ((128, 4), (32, 2), (8, 1))
 
 def _texture_values(H: int, W: int, seed: int, octaves, r0: int, r1: int) -> np.ndarray:
     """Sum over octaves of integer-bilinear lattice noise, rows [r0, r1)."""
-    ys = np.arange(r0, r1, dtype=np.int64)[:, None]
-    xs = np.arange(W, dtype=np.int64)[None, :]
-    acc = np.zeros((r1 - r0, W), dtype=np.int64)
+    ys = np.arange(r0, r1, dtype=np.int64)
+    xs = np.arange(W, dtype=np.int64)
+    acc = np.zeros((r1 - r0, W), dtype=np.int32)
     for k, (c, w) in enumerate(octaves):
-        lat = _lattice(seed * 1000003 + k, H // c + 2, W // c + 2)
-        iy, fy = ys // c, ys % c
-        ix, fx = xs // c, xs % c
-        v = (lat[iy, ix] * (c - fx) * (c - fy) + lat[iy, ix + 1] * fx * (c - fy)
-             + lat[iy + 1, ix] * (c - fx) * fy + lat[iy + 1, ix + 1] * fx * fy) // (c * c)
-        acc += w * v
+        lat = _lattice(seed * 1000003 + k, H // c + 2, W // c + 2).astype(np.int32)
+        iy, fy = ys // c, (ys % c).astype(np.int32)
+        ix, fx = xs // c, (xs % c).astype(np.int32)
+        j0, j1 = int(iy[0]), int(iy[-1]) + 2
+        # separable integer bilinear: along x on the lattice rows, then along y
+        lx = lat[j0:j1, ix] * (c - fx) + lat[j0:j1, ix + 1] * fx
+        rows = iy - j0
+        v = (lx[rows] * (c - fy)[:, None] + lx[rows + 1] * fy[:, None]) // (c * c)
+        acc += np.int32(w) * v
     return acc
 
 
@@ -200,13 +203,14 @@ def uniform(H: int, W: int, value: int = 255) -> np.ndarray:
     return np.full((H, W), value, dtype=np.uint8)
 
 
-def frames(B: int, H: int, W: int, seed0: int = 4000) -> np.ndarray:
-    """Video-like batch (config C4): frame f is texture(seed0+f) thresholded at a
-    density cycling through 0.2..0.6."""
+def frames(B: int, H: int, W: int, seed0: int = 4000, first: int = 0) -> np.ndarray:
+    """Video-like batch (config C4): frame f (= first .. first+B-1) is
+    texture(seed0+f) thresholded at a density cycling through 0.2..0.6."""
     dens = (0.2, 0.3, 0.4, 0.5, 0.6)
     out = np.empty((B, H, W), dtype=np.uint8)
-    for f in range(B):
-        out[f] = texture(H, W, seed0 + f, dens[f % len(dens)], octaves=((64, 4), (16, 2), (4, 1)))
+    for i in range(B):
+        f = first + i
+        out[i] = texture(H, W, seed0 + f, dens[f % len(dens)], octaves=((64, 4), (16, 2), (4, 1)))
     return out
 
 
