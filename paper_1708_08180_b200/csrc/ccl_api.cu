@@ -18,7 +18,7 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes;
+    size_t G_bytes, bits_bytes, runs_bytes;
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -45,6 +45,10 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.nwords = H * int64_t(p.g.WW);
     p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
+    // per-run records: capacity of the worst case (alternating pixels) for the
+    // tallest tile config, so the size does not depend on tile_rows
+    const size_t rows32 = size_t((H + 31) / 32) * 32;
+    p.runs_bytes = align_up(size_t(B) * size_t(p.g.tiles_x) * rows32 * (ccl::kTileW / 2) * sizeof(uint16_t));
     return CCL_OK;
 }
 
@@ -87,11 +91,12 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     const ccl::Geom& g = p.g;
     int32_t* G = static_cast<int32_t*>(ws);
     uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes);
+    uint16_t* runs = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes);
     const long long ntiles = (long long)g.B * g.tiles_x * g.tiles_y;
     if (ntiles == 0) return cudaSuccess;
     const size_t smem = smem_bytes<TY>();
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(img, g, bits, G);
+        ccl::k_local_merge<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(img, g, bits, G, runs);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
@@ -105,7 +110,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         }
     }
     if (stages & kK3) {
-        ccl::k_link<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(g, bits, G, out);
+        ccl::k_link<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(g, bits, G, runs, out);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -150,7 +155,7 @@ ccl_status_t validate_buffers(const Plan& p, const uint8_t* img, const int32_t* 
     if ((stages & kK1) && !img) return CCL_ERR_NULL;
     if ((stages & kK3) && !out) return CCL_ERR_NULL;
     if (!ws) return CCL_ERR_NULL;
-    if (ws_bytes < p.G_bytes + p.bits_bytes) return CCL_ERR_WORKSPACE;
+    if (ws_bytes < p.G_bytes + p.bits_bytes + p.runs_bytes) return CCL_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(ws) % 4) return CCL_ERR_WORKSPACE;
     if (img && out && overlaps(img, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
     if (img && overlaps(img, n, ws, ws_bytes)) return CCL_ERR_ALIAS;
@@ -168,7 +173,7 @@ ccl_status_t label_alloc(const uint8_t* images, int64_t B, int64_t H, int64_t W,
     const size_t n = size_t(B) * size_t(p.g.npx);
     if (overlaps(images, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
     void* ws = nullptr;
-    const size_t bytes = p.G_bytes + p.bits_bytes;
+    const size_t bytes = p.G_bytes + p.bits_bytes + p.runs_bytes;
     cudaError_t e = cudaMallocAsync(&ws, bytes, 0);
     if (e != cudaSuccess) return cuda_fail(e);
     st = run(p, conn, kAll, images, out, ws, 0);
@@ -201,7 +206,7 @@ int ccl_last_cuda_error(void) { return g_last_cuda_error; }
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity) {
     Plan p;
     if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
-    return p.G_bytes + p.bits_bytes;
+    return p.G_bytes + p.bits_bytes + p.runs_bytes;
 }
 
 ccl_status_t ccl_label(const uint8_t* image, int64_t H, int64_t W, int connectivity,
@@ -281,7 +286,7 @@ size_t ccl_host_scratch_bytes(int64_t B, int64_t H, int64_t W, int connectivity)
     Plan p;
     if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
     const size_t n = size_t(B) * size_t(p.g.npx);
-    return align_up(n) + align_up(n * sizeof(int32_t)) + p.G_bytes + p.bits_bytes;
+    return align_up(n) + align_up(n * sizeof(int32_t)) + p.G_bytes + p.bits_bytes + p.runs_bytes;
 }
 
 ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H, int64_t W,

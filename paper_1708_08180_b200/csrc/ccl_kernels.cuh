@@ -36,7 +36,7 @@ namespace ccl {
 
 constexpr int kTileW = 1024;   // pixels per tile row
 constexpr int kWords = 32;     // 32-bit mask words per tile row
-constexpr int kThreads = 512;  // threads per K1/K3 block
+constexpr int kThreads = 256;  // threads per K1/K3 block
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
@@ -50,15 +50,30 @@ struct Geom {
     long long nwords;  // H*WW (per image)
 };
 
+// One 32-px mask word with its row-run description (one 128-bit smem load).
+struct __align__(16) Word {
+    uint32_t m;  // foreground mask
+    uint32_t s;  // run-start mask (tile-local runs)
+    int32_t c;   // x (0..1023) of the run start owning bit 0 of the word (if fg), else -1
+    int32_t pad;
+};
+
 // Shared-memory layout of one K1/K3 tile (dynamic shared memory).
 template <int TY>
 struct TileSmem {
-    uint32_t m[TY][kWords];     // foreground masks
-    uint32_t s[TY][kWords];     // run-start masks (tile-local runs)
-    int32_t c[TY][kWords];      // x (0..1023) of the run start owning bit 0 of the word (if fg)
+    Word wd[TY][kWords];        // .pad = row-local index of the word's first run
     int32_t P[TY * kTileW / 2]; // parent: index (l>>1), value = tile-local index l of parent
-    uint32_t flag[TY * kTileW / 64];  // K3: "root touches a tile edge" bits, index (l>>1)
+    uint32_t flag[TY * kTileW / 64];  // "root touches a tile edge" bits, index (l>>1)
+    int32_t rcnt[TY];           // runs per tile row
 };
+
+// Per-run record written by K1 and read by K3 (uint16 per run, runs of a tile
+// in raster order of their starts): bits 0..14 = tile-local index of the run's
+// local root, bit 15 = that root's component touches a tile edge (so its final
+// label must be resolved through the global parent array G).
+constexpr int kRunEdgeBit = 0x8000;
+template <int TY>
+__host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t nz4(uint32_t w) {
@@ -89,10 +104,10 @@ __device__ __forceinline__ int ld_volatile(const int32_t* p) {
 
 // x (0..1023) of the start of the tile-local run containing foreground pixel x
 // of a tile row described by start masks s[] and carries c[].
-__device__ __forceinline__ int run_start_x(const uint32_t* s, const int32_t* c, int x) {
+__device__ __forceinline__ int run_start_x(const Word* row, int x) {
     const int w = x >> 5, bit = x & 31;
-    const uint32_t below = s[w] & (kFull >> (31 - bit));
-    return below ? ((w << 5) + 31 - __clz(below)) : c[w];
+    const uint32_t below = row[w].s & (kFull >> (31 - bit));
+    return below ? ((w << 5) + 31 - __clz(below)) : row[w].c;
 }
 
 // Row-run analysis of one 1024-px tile row held one word per lane: start mask
@@ -114,7 +129,24 @@ __device__ __forceinline__ void row_runs(uint32_t m, int lane, uint32_t& s, int&
 
 // ----------------------------------------------- shared-memory union-find
 // find / merge of §2.1.3 over tile-local run-start indices.
-__device__ __forceinline__ int find_s(const int32_t* P, int a) {
+// Path halving: every visited node is re-pointed at its grandparent (an
+// ancestor, so set membership never changes; values only move toward roots).
+__device__ __forceinline__ int find_s(int32_t* P, int a) {
+    volatile int32_t* V = P;
+    int p = V[a >> 1];
+    while (p != a) {
+        const int gp = V[p >> 1];
+        if (gp != p) V[a >> 1] = gp;
+        a = p;
+        p = gp;
+    }
+    return a;
+}
+
+// Read-only find: used by the flatten phase, which must leave every run start
+// pointing at its root (a concurrent halving store could otherwise overwrite a
+// flattened entry with a non-root ancestor).
+__device__ __forceinline__ int find_s_ro(const int32_t* P, int a) {
     const volatile int32_t* V = P;
     int p = V[a >> 1];
     while (p != a) {
@@ -140,11 +172,19 @@ __device__ __forceinline__ void union_s(int32_t* P, int a, int b) {
 }
 
 // -------------------------------------------------- global union-find (K2)
-__device__ __forceinline__ int find_g(const int32_t* G, int a) {
+__device__ __forceinline__ void st_volatile(int32_t* p, int v) {
+    *reinterpret_cast<volatile int32_t*>(p) = v;
+}
+
+// find with path halving in global memory (safe under concurrent min-unions:
+// a halving store writes an ancestor of a non-root node, R11).
+__device__ __forceinline__ int find_g(int32_t* G, int a) {
     int p = ld_volatile(G + a);
     while (p != a) {
+        const int gp = ld_volatile(G + p);
+        if (gp != p) st_volatile(G + a, gp);
         a = p;
-        p = ld_volatile(G + a);
+        p = gp;
     }
     return a;
 }
@@ -167,12 +207,13 @@ struct TileId {
 };
 
 template <int TY>
-__device__ __forceinline__ TileId decode_tile(const Geom& g, long long t) {
+__device__ __forceinline__ TileId decode_tile(const Geom& g, unsigned t) {
     TileId id;
-    id.tx = int(t % g.tiles_x);
-    t /= g.tiles_x;
-    id.ty = int(t % g.tiles_y);
-    id.b = int(t / g.tiles_y);
+    const unsigned q = t / unsigned(g.tiles_x);
+    id.tx = int(t - q * unsigned(g.tiles_x));
+    const unsigned q2 = q / unsigned(g.tiles_y);
+    id.ty = int(q - q2 * unsigned(g.tiles_y));
+    id.b = int(q2);
     id.x0 = id.tx * kTileW;
     id.y0 = id.ty * TY;
     return id;
@@ -181,29 +222,60 @@ __device__ __forceinline__ TileId decode_tile(const Geom& g, long long t) {
 // ------------------------------------------- K1 / K3 shared local labeling
 // Phase L1: masks -> smem, run starts, carries, parent init.  `m` is this
 // lane's mask word of tile row r.
-template <int TY>
+template <int TY, bool INIT_P>
 __device__ __forceinline__ void tile_row_init(TileSmem<TY>& sm, int r, int lane, uint32_t m) {
     uint32_t s;
     int c;
     row_runs(m, lane, s, c);
-    sm.m[r][lane] = m;
-    sm.s[r][lane] = s;
-    sm.c[r][lane] = c;
-    const int base = r * kTileW + (lane << 5);
-    uint32_t t = s;
-    while (t) {
-        const int bit = __ffs(t) - 1;
-        t &= t - 1;
-        const int l = base + bit;
-        sm.P[l >> 1] = l;
+    // row-local run index of this word's first run start (exclusive prefix)
+    const int n = __popc(s);
+    int incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+    }
+    Word wd;
+    wd.m = m;
+    wd.s = s;
+    wd.c = c;
+    wd.pad = incl - n;
+    sm.wd[r][lane] = wd;
+    if (lane == 31) sm.rcnt[r] = incl;
+    if (INIT_P) {
+        const int base = r * kTileW + (lane << 5);
+        uint32_t t = s;
+        while (t) {
+            const int bit = __ffs(t) - 1;
+            t &= t - 1;
+            const int l = base + bit;
+            sm.P[l >> 1] = l;
+        }
     }
 }
 
-// Phase L2: local UF between tile rows r-1 and r (Alg. 1 l.25-33 generalised to
-// run pairs; 8-conn adds the diagonal run contacts, reading R2/R10).
-template <int TY, int CONN>
-__device__ __forceinline__ void tile_row_unions(TileSmem<TY>& sm, int r, int lane) {
-    const uint32_t cur = sm.m[r][lane], up = sm.m[r - 1][lane];
+// Tile-local index of the first run of tile row r (prefix of rcnt; after a
+// barrier that follows tile_row_init of all rows).
+template <int TY>
+__device__ __forceinline__ int row_run_base(const TileSmem<TY>& sm, int r, int lane) {
+    int v = lane < TY ? sm.rcnt[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += t;
+    }
+    const int incl = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0);
+    return r > 0 ? incl : 0;
+}
+
+// Every adjacency between a run of tile row r and a run of row r-1 yields one
+// event f(cs, us) (cs, us = tile-local indices of the two run starts): the
+// start of each overlap segment (4-conn, Alg. 1 l.14-18 / l.27-29 at run
+// granularity) plus, for 8-conn, the diagonal run contacts NE / NW that do not
+// overlap (reading R2/R10).  Out-of-tile neighbours count as background.
+template <int TY, int CONN, typename F>
+__device__ __forceinline__ void for_each_row_event(const TileSmem<TY>& sm, int r, int lane, F f) {
+    const uint32_t cur = sm.wd[r][lane].m, up = sm.wd[r - 1][lane].m;
     uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
     uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
     if (lane == 0) { curL = 0; upL = 0; }
@@ -211,14 +283,12 @@ __device__ __forceinline__ void tile_row_unions(TileSmem<TY>& sm, int r, int lan
     const uint32_t o = cur & up, oL = curL & upL;
     uint32_t ev = o & ~((o << 1) | (oL >> 31));  // overlap-segment starts
     const int rb = r * kTileW, ub = (r - 1) * kTileW, xb = lane << 5;
-    const uint32_t* sc = sm.s[r];
-    const int32_t* cc = sm.c[r];
-    const uint32_t* su = sm.s[r - 1];
-    const int32_t* cu = sm.c[r - 1];
+    const Word* wc = sm.wd[r];
+    const Word* wu = sm.wd[r - 1];
     while (ev) {
         const int x = xb + __ffs(ev) - 1;
         ev &= ev - 1;
-        union_s(sm.P, rb + run_start_x(sc, cc, x), ub + run_start_x(su, cu, x));
+        f(rb + run_start_x(wc, x), ub + run_start_x(wu, x));
     }
     if (CONN == 8) {
         const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
@@ -228,37 +298,72 @@ __device__ __forceinline__ void tile_row_unions(TileSmem<TY>& sm, int r, int lan
         while (ne) {
             const int x = xb + __ffs(ne) - 1;
             ne &= ne - 1;
-            union_s(sm.P, rb + run_start_x(sc, cc, x), ub + x + 1);
+            f(rb + run_start_x(wc, x), ub + x + 1);
         }
         while (nw) {
             const int x = xb + __ffs(nw) - 1;
             nw &= nw - 1;
-            union_s(sm.P, rb + x, ub + run_start_x(su, cu, x - 1));
+            f(rb + x, ub + run_start_x(wu, x - 1));
         }
     }
 }
 
-// Phase L3: flatten -- every run start points at its local root.
-template <int TY>
-__device__ __forceinline__ void tile_row_flatten(TileSmem<TY>& sm, int r, int lane) {
-    uint32_t t = sm.s[r][lane];
+// Calls f(l) for every run start l of tile row r held by this lane.
+template <int TY, typename F>
+__device__ __forceinline__ void for_each_run_start(const TileSmem<TY>& sm, int r, int lane, F f) {
+    uint32_t t = sm.wd[r][lane].s;
     const int base = r * kTileW + (lane << 5);
-    volatile int32_t* V = sm.P;
     while (t) {
         const int bit = __ffs(t) - 1;
         t &= t - 1;
-        const int l = base + bit;
-        V[l >> 1] = find_s(sm.P, l);
+        f(base + bit);
     }
 }
 
-// Run the local labeling of one tile whose masks are already in smem.
-template <int TY, int CONN>
+// Local merge of one tile whose masks / runs / P are initialised in smem.
+// Coarse labeling: the row scan + row unification of Alg. 1 (l.9-13, l.19-24
+// in the row direction) is exact here -- every pixel's provisional label is
+// its run start, the lowest equivalent label of its row segment.
+// COARSE_COLUMN additionally performs the column scan (l.14-18) at run
+// granularity before the local UF:
+//  L2 every run takes as parent the leftmost run of the row above it touches
+//     (atomicMin of upper run starts: lower indices, so P[l] <= l throughout);
+//  L3 row-column unification: every run walks its parent chain to its end and
+//     records it (chains bounded by TY);
+//  L4 local UF (Alg. 1 l.25-33) on the remaining adjacencies, most of which are
+//     dismissed by one comparison of the coarse labels.
+// Without COARSE_COLUMN, L4 runs directly on the run adjacencies (measured
+// faster on B200).  L5 flattens: every run start
+// points at its local root.
+template <int TY, int CONN, bool COARSE_COLUMN = false>
 __device__ __forceinline__ void tile_local_uf(TileSmem<TY>& sm, int warp, int lane) {
     __syncthreads();
-    for (int r = warp + 1; r < TY; r += kWarps) tile_row_unions<TY, CONN>(sm, r, lane);
+    volatile int32_t* V = sm.P;
+    if (COARSE_COLUMN) {
+        for (int r = warp + 1; r < TY; r += kWarps)
+            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) { atomicMin(&sm.P[cs >> 1], us); });
+        __syncthreads();
+        for (int r = warp + 1; r < TY; r += kWarps)
+            for_each_run_start<TY>(sm, r, lane, [&](int l) {
+                int t = l, p = V[l >> 1];
+                while (p != t) {
+                    t = p;
+                    p = V[t >> 1];
+                    V[l >> 1] = t;
+                }
+            });
+        __syncthreads();
+        for (int r = warp + 1; r < TY; r += kWarps)
+            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) {
+                if (V[cs >> 1] != V[us >> 1]) union_s(sm.P, cs, us);
+            });
+    } else {
+        for (int r = warp + 1; r < TY; r += kWarps)
+            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) { union_s(sm.P, cs, us); });
+    }
     __syncthreads();
-    for (int r = warp; r < TY; r += kWarps) tile_row_flatten<TY>(sm, r, lane);
+    for (int r = warp; r < TY; r += kWarps)
+        for_each_run_start<TY>(sm, r, lane, [&](int l) { V[l >> 1] = find_s_ro(sm.P, l); });
     __syncthreads();
 }
 
@@ -274,7 +379,7 @@ __device__ __forceinline__ void for_each_edge_item(const TileSmem<TY>& sm, const
                                                    const TileId& id, int warp, int lane, F f) {
     const int rows = min(TY, g.H - id.y0);
     if (warp == 0 && id.y0 > 0) {
-        uint32_t t = sm.s[0][lane];
+        uint32_t t = sm.wd[0][lane].s;
         while (t) {
             const int bit = __ffs(t) - 1;
             t &= t - 1;
@@ -282,7 +387,7 @@ __device__ __forceinline__ void for_each_edge_item(const TileSmem<TY>& sm, const
             f(l, l);
         }
     } else if (warp == 1 && id.y0 + TY < g.H) {
-        uint32_t t = sm.s[TY - 1][lane];
+        uint32_t t = sm.wd[TY - 1][lane].s;
         while (t) {
             const int bit = __ffs(t) - 1;
             t &= t - 1;
@@ -291,11 +396,11 @@ __device__ __forceinline__ void for_each_edge_item(const TileSmem<TY>& sm, const
         }
     } else if (warp == 2 && id.x0 > 0) {
         for (int r = lane; r < rows; r += 32)
-            if (sm.m[r][0] & 1u) f(r * kTileW, r * kTileW);
+            if (sm.wd[r][0].m & 1u) f(r * kTileW, r * kTileW);
     } else if (warp == 3 && id.x0 + kTileW < g.W) {
         for (int r = lane; r < rows; r += 32)
-            if (sm.m[r][kWords - 1] >> 31)
-                f(r * kTileW + kTileW - 1, r * kTileW + run_start_x(sm.s[r], sm.c[r], kTileW - 1));
+            if (sm.wd[r][kWords - 1].m >> 31)
+                f(r * kTileW + kTileW - 1, r * kTileW + run_start_x(sm.wd[r], kTileW - 1));
     }
 }
 
@@ -303,7 +408,8 @@ __device__ __forceinline__ void for_each_edge_item(const TileSmem<TY>& sm, const
 template <int TY, int CONN, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                           uint32_t* __restrict__ bits,
-                                                          int32_t* __restrict__ G) {
+                                                          int32_t* __restrict__ G,
+                                                          uint16_t* __restrict__ R) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -311,6 +417,7 @@ __global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restr
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
 
+    for (int i = threadIdx.x; i < TY * kTileW / 64; i += kThreads) sm.flag[i] = 0;
     // Alg. 1 l.3-8: load the tile (out-of-image pixels read as background, R5)
     for (int r = warp; r < TY; r += kWarps) {
         const int y = id.y0 + r;
@@ -338,11 +445,12 @@ __global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restr
         }
         const int wg = id.tx * kWords + lane;
         if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
-        tile_row_init<TY>(sm, r, lane, m);
+        tile_row_init<TY, true>(sm, r, lane, m);
     }
     tile_local_uf<TY, CONN>(sm, warp, lane);
 
-    // Alg. 1 l.34-39 for tile-edge items only: G[g(l)] = g(root), G[g(root)] = g(root)
+    // Alg. 1 l.34-39 for tile-edge items only: G[g(l)] = g(root), G[g(root)] = g(root);
+    // and flag the roots whose component touches a tile edge
     int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     for_each_edge_item<TY>(sm, g, id, warp, lane, [&](int l, int ls) {
@@ -351,19 +459,56 @@ __global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restr
         const int gr = (y0 + (root >> 10)) * W + x0 + (root & 1023);
         Gb[gl] = gr;
         Gb[gr] = gr;
+        atomicOr(&sm.flag[root >> 6], 1u << ((root >> 1) & 31));
     });
+    __syncthreads();
+    // per-run records for K3 (local root + edge flag), runs in raster order
+    uint16_t* Rt = R + size_t(blockIdx.x) * runs_per_tile_cap<TY>();
+    for (int r = warp; r < TY; r += kWarps) {
+        const int k0 = row_run_base<TY>(sm, r, lane) + sm.wd[r][lane].pad;
+        int j = 0;
+        for_each_run_start<TY>(sm, r, lane, [&](int l) {
+            const int root = sm.P[l >> 1];
+            const int e = (sm.flag[root >> 6] >> ((root >> 1) & 31)) & 1u;
+            Rt[k0 + j++] = uint16_t(root | (e ? kRunEdgeBit : 0));
+        });
+    }
 }
 
 // ============================================================ K2: boundary
+// Warp-cooperative union of a batch of (run start / edge pixel) index pairs:
+// each lane holds at most one pair (ia, ib) (ia < 0: none).  Step 1 reads the
+// local roots G[ia], G[ib] written by K1 (one independent load per lane);
+// step 2 drops pairs already seen in this warp (identical root pairs are
+// common: two large components meet at many places along a tile edge) so only
+// one lane per distinct pair runs the global min-union.  This keeps the hot
+// root of a giant component from being read once per crossing edge.
+__device__ __forceinline__ void warp_union_pairs(int32_t* G, int ia, int ib, unsigned long long& last,
+                                                 int img) {
+    int a = -1, b = -1;
+    if (ia >= 0) {
+        a = ld_volatile(G + ia);
+        b = ld_volatile(G + ib);
+        if (a > b) { int t = a; a = b; b = t; }
+    }
+    const unsigned long long key =
+        (ia >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
+    // pairs are only equal within one image (G values are image-local indices)
+    const unsigned grp = __match_any_sync(kFull, key) & __match_any_sync(kFull, img);
+    const int lane = threadIdx.x & 31;
+    if (key != ~0ull && key != last && (__ffs(grp) - 1) == lane) union_g(G, a, b);
+    if (key != ~0ull) last = key;
+}
+
 // Horizontal tile edges: one warp per (image, band >= 1, tile column); vertical
-// tile edges: one thread per (image, row, tile column boundary >= 1).
+// tile edges: one thread per (image, tile column boundary >= 1, row).
 template <int TY, int CONN>
 __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
                                                   int32_t* __restrict__ G, long long n_h,
                                                   long long blocks_h) {
-    __shared__ uint32_t s_s[8][2][kWords];
-    __shared__ int32_t s_c[8][2][kWords];
+    __shared__ Word s_w[8][2][kWords];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long last = ~0ull;
     if (blockIdx.x < blocks_h) {
         const long long task = (long long)blockIdx.x * 8 + warp;
         if (task >= n_h) return;  // whole warp exits together
@@ -382,10 +527,8 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         int cc, cu;
         row_runs(cur, lane, sc, cc);
         row_runs(up, lane, su, cu);
-        s_s[warp][0][lane] = sc;
-        s_c[warp][0][lane] = cc;
-        s_s[warp][1][lane] = su;
-        s_c[warp][1][lane] = cu;
+        s_w[warp][0][lane] = Word{cur, sc, cc, 0};
+        s_w[warp][1][lane] = Word{up, su, cu, 0};
         __syncwarp();
         uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
         uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
@@ -393,157 +536,179 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         if (lane == 31) { curR = 0; upR = 0; }
         const uint32_t o = cur & up, oL = curL & upL;
         uint32_t ev = o & ~((o << 1) | (oL >> 31));
-        const int gc = y0 * g.W + x0, gu = (y0 - 1) * g.W + x0, xb = lane << 5;
-        while (ev) {
-            const int x = xb + __ffs(ev) - 1;
-            ev &= ev - 1;
-            union_g(Gb, gc + run_start_x(s_s[warp][0], s_c[warp][0], x),
-                    gu + run_start_x(s_s[warp][1], s_c[warp][1], x));
-        }
+        uint32_t ne = 0, nw = 0;
+        bool cnw = false, cne = false;  // diagonal edges through the tile corners
         if (CONN == 8) {
             const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
             const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
-            uint32_t ne = cur & ~cur_n & ~up & up_n;
-            uint32_t nw = cur & ~cur_p & ~up & up_p;
-            while (ne) {
+            ne = cur & ~cur_n & ~up & up_n;
+            nw = cur & ~cur_p & ~up & up_p;
+            if (lane == 0 && tx > 0 && (cur & 1u)) cnw = bm[size_t(y0 - 1) * g.WW + wg - 1] >> 31;
+            if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = bm[size_t(y0 - 1) * g.WW + wg + 1] & 1u;
+        }
+        const int gc = y0 * g.W + x0, gu = (y0 - 1) * g.W + x0, xb = lane << 5;
+        while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
+            int ia = -1, ib = -1;
+            if (ev) {
+                const int x = xb + __ffs(ev) - 1;
+                ev &= ev - 1;
+                ia = gc + run_start_x(s_w[warp][0], x);
+                ib = gu + run_start_x(s_w[warp][1], x);
+            } else if (ne) {
                 const int x = xb + __ffs(ne) - 1;
                 ne &= ne - 1;
-                union_g(Gb, gc + run_start_x(s_s[warp][0], s_c[warp][0], x), gu + x + 1);
-            }
-            while (nw) {
+                ia = gc + run_start_x(s_w[warp][0], x);
+                ib = gu + x + 1;
+            } else if (nw) {
                 const int x = xb + __ffs(nw) - 1;
                 nw &= nw - 1;
-                union_g(Gb, gc + x, gu + run_start_x(s_s[warp][1], s_c[warp][1], x - 1));
+                ia = gc + x;
+                ib = gu + run_start_x(s_w[warp][1], x - 1);
+            } else if (cnw) {
+                cnw = false;
+                ia = gc;            // (x0, y0)
+                ib = gu - 1;        // (x0-1, y0-1)
+            } else if (cne) {
+                cne = false;
+                ia = gc + kTileW - 1;  // (x0+1023, y0)
+                ib = gu + kTileW;      // (x0+1024, y0-1)
             }
-            // diagonal edges that also cross a vertical tile edge (tile corners)
-            if (lane == 0 && tx > 0 && (cur & 1u)) {
-                const uint32_t upw = bm[size_t(y0 - 1) * g.WW + wg - 1];
-                if (upw >> 31) union_g(Gb, gc, gu - 1);  // NW of (x0, y0)
-            }
-            if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) {
-                const uint32_t upw = bm[size_t(y0 - 1) * g.WW + wg + 1];
-                if (upw & 1u) union_g(Gb, gc + kTileW - 1, gu + kTileW);  // NE of (x0+1023, y0)
-            }
+            warp_union_pairs(Gb, ia, ib, last, 0);
         }
     } else {
         const long long task = (long long)(blockIdx.x - blocks_h) * 256 + threadIdx.x;
         const int nbx = g.tiles_x - 1;
         const long long n_v = (long long)g.B * g.H * nbx;
-        if (task >= n_v) return;
-        long long t = task;
-        const int bx = 1 + int(t % nbx);
-        t /= nbx;
+        const bool valid = task < n_v;
+        long long t = valid ? task : 0;
         const int y = int(t % g.H);
-        const int b = int(t / g.H);
+        t /= g.H;
+        const int bx = 1 + int(t % nbx);
+        const int b = int(t / nbx);
         const int x0 = bx * kTileW;
         const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
         int32_t* Gb = G + size_t(b) * size_t(g.npx);
         const int wl = bx * kWords - 1;
         const size_t row = size_t(y) * g.WW;
-        const bool L = bm[row + wl] >> 31, R = bm[row + wl + 1] & 1u;
+        bool L = false, R = false, Lu = false, Ru = false;
+        if (valid) {
+            L = bm[row + wl] >> 31;
+            R = bm[row + wl + 1] & 1u;
+            if (CONN == 8 && (y % TY) != 0 && (L || R)) {
+                Lu = bm[row - g.WW + wl] >> 31;
+                Ru = bm[row - g.WW + wl + 1] & 1u;
+            }
+        }
         const int p = y * g.W + x0;
-        if (L && R) union_g(Gb, p - 1, p);  // W edge of (x0, y)
-        if (CONN == 8 && (y % TY) != 0 && (L || R)) {
-            const size_t rowu = row - g.WW;
-            const bool Lu = bm[rowu + wl] >> 31, Ru = bm[rowu + wl + 1] & 1u;
-            if (R && Lu) union_g(Gb, p, p - g.W - 1);  // NW of (x0, y)
-            if (L && Ru) union_g(Gb, p - 1, p - g.W);  // NE of (x0-1, y)
+        warp_union_pairs(Gb, (L && R) ? p - 1 : -1, p, last, b);              // W edge of (x0, y)
+        if (CONN == 8) {
+            warp_union_pairs(Gb, (R && Lu) ? p : -1, p - g.W - 1, last, b);   // NW of (x0, y)
+            warp_union_pairs(Gb, (L && Ru) ? p - 1 : -1, p - g.W, last, b);   // NE of (x0-1, y)
         }
     }
 }
 
 // ================================================================ K3: link
+// Final link (§2.3): the tile's runs are re-derived from the bit mask (run
+// starts only, no union-find) and take their local root from K1's per-run
+// records; roots whose component touches a tile edge are resolved through G
+// (find); then every pixel gets 1 + its global root, or 0.
 template <int TY, int CONN, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_link(Geom g, const uint32_t* __restrict__ bits,
-                                                   const int32_t* __restrict__ G,
+                                                   int32_t* __restrict__ G,
+                                                   const uint16_t* __restrict__ R,
                                                    int32_t* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const TileId id = decode_tile<TY>(g, blockIdx.x);
     const uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
-    const int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
+    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
     int32_t* ob = out + size_t(id.b) * size_t(g.npx);
+    const uint16_t* Rt = R + size_t(blockIdx.x) * runs_per_tile_cap<TY>();
 
-    for (int i = threadIdx.x; i < TY * kTileW / 64; i += kThreads) sm.flag[i] = 0;
     for (int r = warp; r < TY; r += kWarps) {
         const int y = id.y0 + r;
         const int wg = id.tx * kWords + lane;
         const uint32_t m = (y < g.H && wg < g.WW) ? __ldg(bm + size_t(y) * g.WW + wg) : 0u;
-        tile_row_init<TY>(sm, r, lane, m);
+        tile_row_init<TY, false>(sm, r, lane, m);
     }
-    tile_local_uf<TY, CONN>(sm, warp, lane);
-
-    // mark roots of tile-edge items (exactly the roots K1 initialised in G)
-    for_each_edge_item<TY>(sm, g, id, warp, lane, [&](int, int ls) {
-        const int root = sm.P[ls >> 1];
-        atomicOr(&sm.flag[root >> 6], 1u << ((root >> 1) & 31));
-    });
     __syncthreads();
 
-    // pass A: every local root -> tagged final label 1 + global root
+    // pass A: P[l] <- local root (untagged) for non-roots; roots get their
+    // tagged final label 1 + global root
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     for (int r = warp; r < TY; r += kWarps) {
-        uint32_t t = sm.s[r][lane];
-        const int base = r * kTileW + (lane << 5);
-        while (t) {
-            const int bit = __ffs(t) - 1;
-            t &= t - 1;
-            const int l = base + bit;
-            if (sm.P[l >> 1] == l) {
+        const int k0 = row_run_base<TY>(sm, r, lane) + sm.wd[r][lane].pad;
+        int j = 0;
+        for_each_run_start<TY>(sm, r, lane, [&](int l) {
+            const int v = __ldg(Rt + k0 + j++);
+            const int root = v & (kRunEdgeBit - 1);
+            if (root == l) {
                 int gr = (y0 + r) * W + x0 + (l & 1023);
-                if ((sm.flag[l >> 6] >> ((l >> 1) & 31)) & 1u) gr = find_g(Gb, gr);
+                if (v & kRunEdgeBit) gr = find_g(Gb, gr);
                 sm.P[l >> 1] = (gr + 1) | kTag;
+            } else {
+                sm.P[l >> 1] = root;
             }
-        }
+        });
     }
     __syncthreads();
     // pass B: non-root run starts take their root's tagged label
-    for (int r = warp; r < TY; r += kWarps) {
-        uint32_t t = sm.s[r][lane];
-        const int base = r * kTileW + (lane << 5);
-        while (t) {
-            const int bit = __ffs(t) - 1;
-            t &= t - 1;
-            const int l = base + bit;
+    for (int r = warp; r < TY; r += kWarps)
+        for_each_run_start<TY>(sm, r, lane, [&](int l) {
             const int p = sm.P[l >> 1];
             if (p >= 0) sm.P[l >> 1] = sm.P[p >> 1];
-        }
-    }
+        });
     __syncthreads();
 
-    // stream the labels: lane writes 4 consecutive pixels per step
+    // stream the labels; every run-start entry of P now holds its tagged label
     for (int r = warp; r < TY; r += kWarps) {
         const int y = y0 + r;
         if (y >= g.H) break;
         int32_t* orow = ob + size_t(y) * size_t(W) + x0;
         const int rb = r * kTileW;
         if (VEC) {
+            // lane writes 4 consecutive pixels per step (512 B per warp store)
 #pragma unroll 2
             for (int j = 0; j < kTileW / 128; ++j) {
                 const int x = 128 * j + 4 * lane;
                 if (x0 + x >= W) break;
                 const int w = x >> 5, sh = x & 31;
-                const uint32_t m = sm.m[r][w], s = sm.s[r][w];
-                const int c = sm.c[r][w];
-                int v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int bit = sh + k;
-                    const uint32_t below = s & (kFull >> (31 - bit));
-                    const int st = below ? ((w << 5) + 31 - __clz(below)) : c;
-                    v[k] = ((m >> bit) & 1u) ? (sm.P[(rb + st) >> 1] & 0x7FFFFFFF) : 0;
+                const Word wd = sm.wd[r][w];
+                const uint32_t fgn = (wd.m >> sh) & 0xFu;
+                int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+                if (fgn) {
+                    const uint32_t stn = (wd.s >> sh) & 0xFu;
+                    int cur = 0;
+                    if (fgn & 1u) {
+                        const uint32_t below = wd.s & (kFull >> (31 - sh));
+                        const int st = below ? ((w << 5) + 31 - __clz(below)) : wd.c;
+                        cur = sm.P[(rb + st) >> 1];
+                    }
+                    const int pb = (rb + x) >> 1;  // P index of pixel x+1 / x+2 / x+3 starts
+                    v0 = cur;
+                    if (stn & 2u) cur = sm.P[pb];          // start at x+1: (rb+x+1)>>1 == pb
+                    v1 = cur;
+                    if (stn & 4u) cur = sm.P[pb + 1];      // start at x+2
+                    v2 = cur;
+                    if (stn & 8u) cur = sm.P[pb + 1];      // start at x+3: (rb+x+3)>>1 == pb+1
+                    v3 = cur;
+                    v0 = (fgn & 1u) ? (v0 & 0x7FFFFFFF) : 0;
+                    v1 = (fgn & 2u) ? (v1 & 0x7FFFFFFF) : 0;
+                    v2 = (fgn & 4u) ? (v2 & 0x7FFFFFFF) : 0;
+                    v3 = (fgn & 8u) ? (v3 & 0x7FFFFFFF) : 0;
                 }
-                st_stream_i4(orow + x, v[0], v[1], v[2], v[3]);
+                st_stream_i4(orow + x, v0, v1, v2, v3);
             }
         } else {
             for (int k = 0; k < kWords; ++k) {
                 const int x = (k << 5) + lane;
                 if (x0 + x < W) {
-                    const uint32_t m = sm.m[r][k];
+                    const uint32_t m = sm.wd[r][k].m;
                     int v = 0;
                     if ((m >> lane) & 1u) {
-                        const int st = run_start_x(sm.s[r], sm.c[r], x);
+                        const int st = run_start_x(sm.wd[r], x);
                         v = sm.P[(rb + st) >> 1] & 0x7FFFFFFF;
                     }
                     orow[x] = v;
