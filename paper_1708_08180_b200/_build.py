@@ -39,12 +39,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
+    """check=True compiles device-side bounds assertions (-DCCL_CHECK)."""
     if not force and not needs_build():
         return LIB
     cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *cu, "-o", tmp]
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DCCL_CHECK"] if check else []), "-I", os.path.join(ROOT, "include"), *cu,
+           "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
@@ -58,4 +60,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, check="--check" in sys.argv))

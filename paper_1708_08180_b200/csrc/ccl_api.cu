@@ -18,7 +18,8 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes, runs_bytes;
+    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes;
+    size_t total() const { return G_bytes + bits_bytes + runs_bytes + 2 * edge_bytes; }
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -43,12 +44,18 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.tiles_y = int((H + tile_rows - 1) / tile_rows);
     p.g.npx = H * W;
     p.g.nwords = H * int64_t(p.g.WW);
+    p.g.div_tx = ccl::FastDiv(unsigned(p.g.tiles_x));
+    p.g.div_ty = ccl::FastDiv(unsigned(p.g.tiles_y));
     p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
     // per-run records: capacity of the worst case (alternating pixels) for the
     // tallest tile config, so the size does not depend on tile_rows
     const size_t rows32 = size_t((H + 31) / 32) * 32;
-    p.runs_bytes = align_up(size_t(B) * size_t(p.g.tiles_x) * rows32 * (ccl::kTileW / 2) * sizeof(uint16_t));
+    p.runs_bytes = align_up(size_t(B) * size_t(p.g.tiles_x) * rows32 * (ccl::kTileW / 2) * sizeof(uint32_t));
+    // edge-root lists E and resolved labels F: kEdgeCap ints per tile, sized
+    // for the most tiles any config makes (tile_rows = 8)
+    const size_t tiles8 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 7) / 8);
+    p.edge_bytes = align_up(tiles8 * ccl::kEdgeCap * sizeof(int32_t));
     return CCL_OK;
 }
 
@@ -65,6 +72,8 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 
 template <int TY>
 size_t smem_bytes() { return sizeof(ccl::TileSmem<TY>); }
+template <int TY>
+size_t smem_bytes_k1() { return sizeof(ccl::K1Smem<TY>); }
 
 template <int TY, int CONN, bool VEC>
 cudaError_t setup_attrs() {
@@ -72,7 +81,7 @@ cudaError_t setup_attrs() {
     static cudaError_t once = [] {
         cudaError_t e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem_bytes<TY>()));
+                                             int(smem_bytes_k1<TY>()));
         if (e != cudaSuccess) return e;
         return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -83,6 +92,29 @@ cudaError_t setup_attrs() {
 
 enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7 };
 
+// Resident blocks per device for the persistent kernels K1 (which = 1) and
+// K3 (which = 3): SMs x blocks per SM at full occupancy, cached per
+// instantiation and device.
+template <int TY, int CONN, bool VEC>
+int persistent_blocks(int which) {
+    static int cached[2][64] = {{0}};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    const int w = which == 1 ? 0 : 1;
+    if (cached[w][dev]) return cached[w][dev];
+    int sms = 0, b = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (which == 1)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads,
+                                                      smem_bytes_k1<TY>());
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC>, ccl::kThreads,
+                                                      smem_bytes<TY>());
+    cached[w][dev] = std::max(1, sms) * std::max(1, b);
+    return cached[w][dev];
+}
+
 template <int TY, int CONN, bool VEC>
 cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* out, void* ws,
                        cudaStream_t s) {
@@ -91,12 +123,18 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     const ccl::Geom& g = p.g;
     int32_t* G = static_cast<int32_t*>(ws);
     uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes);
-    uint16_t* runs = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes);
+    uint32_t* runs = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes);
+    int32_t* E = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes + p.runs_bytes);
+    int32_t* F = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(E) + p.edge_bytes);
     const long long ntiles = (long long)g.B * g.tiles_x * g.tiles_y;
     if (ntiles == 0) return cudaSuccess;
     const size_t smem = smem_bytes<TY>();
+    // persistent K1/K3: one wave of resident blocks walks all tiles
+    const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
+    const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(img, g, bits, G, runs);
+        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads, smem_bytes_k1<TY>(), s>>>(img, g, bits, G, runs, E,
+                                                                                         unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
@@ -104,13 +142,17 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         const long long n_v = (long long)g.B * g.H * (g.tiles_x - 1);
         const long long blocks_h = (n_h + 7) / 8, blocks_v = (n_v + 255) / 256;
         if (blocks_h + blocks_v > 0) {
-            ccl::k_boundary<TY, CONN><<<unsigned(blocks_h + blocks_v), 256, 0, s>>>(g, bits, G, n_h,
+            ccl::k_boundary<TY, CONN><<<unsigned(blocks_h + blocks_v), 256, 0, s>>>(g, bits, runs, E, G, n_h,
                                                                                    blocks_h);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
+        // resolve every tile's edge-touching roots (one warp per tile)
+        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
+        ccl::k_resolve<TY><<<rblocks, 256, 0, s>>>(g, G, E, F, unsigned(ntiles));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK3) {
-        ccl::k_link<TY, CONN, VEC><<<unsigned(ntiles), ccl::kThreads, smem, s>>>(g, bits, G, runs, out);
+        ccl::k_link<TY, CONN, VEC><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -155,7 +197,7 @@ ccl_status_t validate_buffers(const Plan& p, const uint8_t* img, const int32_t* 
     if ((stages & kK1) && !img) return CCL_ERR_NULL;
     if ((stages & kK3) && !out) return CCL_ERR_NULL;
     if (!ws) return CCL_ERR_NULL;
-    if (ws_bytes < p.G_bytes + p.bits_bytes + p.runs_bytes) return CCL_ERR_WORKSPACE;
+    if (ws_bytes < p.total()) return CCL_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(ws) % 4) return CCL_ERR_WORKSPACE;
     if (img && out && overlaps(img, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
     if (img && overlaps(img, n, ws, ws_bytes)) return CCL_ERR_ALIAS;
@@ -173,7 +215,7 @@ ccl_status_t label_alloc(const uint8_t* images, int64_t B, int64_t H, int64_t W,
     const size_t n = size_t(B) * size_t(p.g.npx);
     if (overlaps(images, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
     void* ws = nullptr;
-    const size_t bytes = p.G_bytes + p.bits_bytes + p.runs_bytes;
+    const size_t bytes = p.total();
     cudaError_t e = cudaMallocAsync(&ws, bytes, 0);
     if (e != cudaSuccess) return cuda_fail(e);
     st = run(p, conn, kAll, images, out, ws, 0);
@@ -206,7 +248,7 @@ int ccl_last_cuda_error(void) { return g_last_cuda_error; }
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity) {
     Plan p;
     if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
-    return p.G_bytes + p.bits_bytes + p.runs_bytes;
+    return p.total();
 }
 
 ccl_status_t ccl_label(const uint8_t* image, int64_t H, int64_t W, int connectivity,
@@ -286,7 +328,7 @@ size_t ccl_host_scratch_bytes(int64_t B, int64_t H, int64_t W, int connectivity)
     Plan p;
     if (make_plan(B, H, W, connectivity, 0, p) != CCL_OK) return 0;
     const size_t n = size_t(B) * size_t(p.g.npx);
-    return align_up(n) + align_up(n * sizeof(int32_t)) + p.G_bytes + p.bits_bytes + p.runs_bytes;
+    return align_up(n) + align_up(n * sizeof(int32_t)) + p.total();
 }
 
 ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H, int64_t W,

@@ -29,8 +29,19 @@
 //    for every pixel with 128-bit evict-first stores.  DRAM traffic per pixel
 //    ~ 1 B (image) + 4 B (labels) + 1/4 B (mask) + edge entries.
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#ifdef CCL_CHECK
+#define CCL_ASSERT(c) assert(c)
+#define CCL_LOOP_GUARD(name) int name##_guard = 0
+#define CCL_LOOP_TICK(name) assert(++name##_guard < (1 << 22))
+#else
+#define CCL_ASSERT(c) ((void)0)
+#define CCL_LOOP_GUARD(name) ((void)0)
+#define CCL_LOOP_TICK(name) ((void)0)
+#endif
 
 namespace ccl {
 
@@ -41,6 +52,19 @@ constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
 
+// Division by a runtime-invariant divisor d >= 1 for numerators n < 2^31 via
+// a precomputed multiplier (Granlund-Montgomery): q = (umulhi(n, mul) + n) >> shr.
+struct FastDiv {
+    unsigned d, mul, shr;
+    __host__ __device__ FastDiv() : d(1), mul(0), shr(0) {}
+    __host__ explicit FastDiv(unsigned dd) : d(dd) {
+        shr = 0;
+        while ((1ull << shr) < dd) ++shr;
+        mul = unsigned(((1ull << 32) * ((1ull << shr) - dd)) / dd + 1);
+    }
+    __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, mul) + n) >> shr; }
+};
+
 struct Geom {
     int B, H, W;       // batch, rows, columns
     int WW;            // mask words per image row = ceil(W/32)
@@ -48,6 +72,7 @@ struct Geom {
     int tiles_y;       // ceil(H/TY)
     long long npx;     // H*W  (per image)
     long long nwords;  // H*WW (per image)
+    FastDiv div_tx, div_ty;  // by tiles_x, tiles_y
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -58,22 +83,41 @@ struct __align__(16) Word {
     int32_t pad;
 };
 
-// Shared-memory layout of one K1/K3 tile (dynamic shared memory).
+// Per-run record written by K1 and read by K3 (uint32 per run, runs of a tile
+// in raster order of their starts): bits 0..14 = tile-local index of the run's
+// local root (row*1024 + x of its start); bits 16..31 = 1 + the root's index in
+// the tile's edge-root list if its component touches a tile edge (its final
+// label then comes from the boundary analysis), else 0.
+constexpr int kRunCache = 256;  // run records K3 prefetches per tile
+template <int TY>
+__host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
+// Edge-root list of a tile (written by K1): [0] = count n, [1..n] = image-local
+// raster index of each edge-touching local root, in run order.  The resolved
+// final labels (written by the boundary analysis) live at the same offsets - 1
+// of a parallel array F.  Capacity: <= 512 runs per tile row x 2 rows + 2 TY
+// column pixels; 1120 covers TY <= 32.
+// Per-tile edge block E[t] (kEdgeCap ints), written by K1:
+//   [0] n = number of edge-touching local roots; [1] run id of the first run of
+//   the tile's last row; [kEdgeLC + r] / [kEdgeRC + r] = image-local raster
+//   index of the local root of pixel (r, 0) / (r, 1023), or -1 (background or
+//   no neighbouring tile); [kEdgeList + i], i < n = the edge roots, in run order.
+constexpr int kEdgeLC = 2;
+constexpr int kEdgeRC = 34;
+constexpr int kEdgeList = 66;
+constexpr int kEdgeCap = 1152;
+constexpr int kEdgeCache = 32;  // resolved labels K3 prefetches per tile
+
+// Shared-memory layout of one K3 tile (dynamic shared memory).
 template <int TY>
 struct TileSmem {
     Word wd[TY][kWords];        // .pad = row-local index of the word's first run
-    int32_t P[TY * kTileW / 2]; // parent: index (l>>1), value = tile-local index l of parent
-    uint32_t flag[TY * kTileW / 64];  // "root touches a tile edge" bits, index (l>>1)
+    int32_t P[TY * kTileW / 2]; // index (l>>1) of a run start l: its final label (tagged)
     int32_t rcnt[TY];           // runs per tile row
+    uint32_t rc[kRunCache];     // K3: first run records of the tile (prefetched)
+    int32_t fc[kEdgeCache];     // K3: first resolved edge labels (prefetched)
 };
 
-// Per-run record written by K1 and read by K3 (uint16 per run, runs of a tile
-// in raster order of their starts): bits 0..14 = tile-local index of the run's
-// local root, bit 15 = that root's component touches a tile edge (so its final
-// label must be resolved through the global parent array G).
-constexpr int kRunEdgeBit = 0x8000;
-template <int TY>
-__host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
+
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t nz4(uint32_t w) {
@@ -127,50 +171,6 @@ __device__ __forceinline__ void row_runs(uint32_t m, int lane, uint32_t& s, int&
     c = (m & 1u) ? ((s & 1u) ? (lane << 5) : excl) : -1;
 }
 
-// ----------------------------------------------- shared-memory union-find
-// find / merge of §2.1.3 over tile-local run-start indices.
-// Path halving: every visited node is re-pointed at its grandparent (an
-// ancestor, so set membership never changes; values only move toward roots).
-__device__ __forceinline__ int find_s(int32_t* P, int a) {
-    volatile int32_t* V = P;
-    int p = V[a >> 1];
-    while (p != a) {
-        const int gp = V[p >> 1];
-        if (gp != p) V[a >> 1] = gp;
-        a = p;
-        p = gp;
-    }
-    return a;
-}
-
-// Read-only find: used by the flatten phase, which must leave every run start
-// pointing at its root (a concurrent halving store could otherwise overwrite a
-// flattened entry with a non-root ancestor).
-__device__ __forceinline__ int find_s_ro(const int32_t* P, int a) {
-    const volatile int32_t* V = P;
-    int p = V[a >> 1];
-    while (p != a) {
-        a = p;
-        p = V[a >> 1];
-    }
-    return a;
-}
-
-// Lock-free minimum-root union (reading R11): the larger root is re-pointed at
-// the smaller with atomicMin; if someone else re-linked it first, retry with
-// the value it was linked to.
-__device__ __forceinline__ void union_s(int32_t* P, int a, int b) {
-    while (true) {
-        a = find_s(P, a);
-        b = find_s(P, b);
-        if (a == b) return;
-        if (a < b) { int t = a; a = b; b = t; }
-        const int old = atomicMin(&P[a >> 1], b);
-        if (old == a) return;
-        a = old;
-    }
-}
-
 // -------------------------------------------------- global union-find (K2)
 __device__ __forceinline__ void st_volatile(int32_t* p, int v) {
     *reinterpret_cast<volatile int32_t*>(p) = v;
@@ -189,16 +189,45 @@ __device__ __forceinline__ int find_g(int32_t* G, int a) {
     return a;
 }
 
-__device__ __forceinline__ void union_g(int32_t* G, int a, int b) {
-    while (true) {
-        a = find_g(G, a);
-        b = find_g(G, b);
-        if (a == b) return;
-        if (a < b) { int t = a; a = b; b = t; }
-        const int old = atomicMin(G + a, b);
-        if (old == a) return;
-        a = old;
+// Rem's union with splicing, lock-free (reading R11).  Walk x and y upward in
+// interleaved fashion, always on the side whose parent is larger; at every
+// step re-point that node at the other side's parent with atomicMin (a
+// "splice": it merges the two sets while compressing the path) and continue
+// from the parent it had.  Stop when both nodes have the same parent (same
+// set) or when a root gets linked.  Values only decrease (G[i] <= i), every
+// change links two nodes that must end up in one set, and each step moves to
+// a strictly smaller node, so it terminates; the walk usually meets below the
+// root, so the hot root entry of a giant component is rarely touched.
+__device__ __forceinline__ void union_g(int32_t* G, int x, int y) {
+    int px = ld_volatile(G + x), py = ld_volatile(G + y);
+    CCL_LOOP_GUARD(ug);
+    while (px != py) {
+        CCL_LOOP_TICK(ug);
+        CCL_ASSERT(px <= x && py <= y && px >= 0 && py >= 0);
+        if (px < py) {
+            int t = x; x = y; y = t;
+            t = px; px = py; py = t;
+        }
+        // px > py: node x hangs above py; move it below py
+        const int old = atomicMin(G + x, py);
+        if (old == x) return;  // x was a root: linked
+        x = old;               // keep merging x's former ancestors
+        px = ld_volatile(G + x);
     }
+}
+
+// Read-only find for after all unions are done (L1-cacheable loads: the hot
+// root of a giant component is then served from each SM's L1).
+__device__ __forceinline__ int find_g_ro(const int32_t* G, int a) {
+    int p = __ldg(G + a);
+    CCL_LOOP_GUARD(fg);
+    while (p != a) {
+        CCL_LOOP_TICK(fg);
+        CCL_ASSERT(p >= 0 && p < a);
+        a = p;
+        p = __ldg(G + a);
+    }
+    return a;
 }
 
 // ------------------------------------------------------------- tile decode
@@ -209,9 +238,9 @@ struct TileId {
 template <int TY>
 __device__ __forceinline__ TileId decode_tile(const Geom& g, unsigned t) {
     TileId id;
-    const unsigned q = t / unsigned(g.tiles_x);
+    const unsigned q = g.div_tx.div(t);
     id.tx = int(t - q * unsigned(g.tiles_x));
-    const unsigned q2 = q / unsigned(g.tiles_y);
+    const unsigned q2 = g.div_ty.div(q);
     id.ty = int(q - q2 * unsigned(g.tiles_y));
     id.b = int(q2);
     id.x0 = id.tx * kTileW;
@@ -268,46 +297,6 @@ __device__ __forceinline__ int row_run_base(const TileSmem<TY>& sm, int r, int l
     return r > 0 ? incl : 0;
 }
 
-// Every adjacency between a run of tile row r and a run of row r-1 yields one
-// event f(cs, us) (cs, us = tile-local indices of the two run starts): the
-// start of each overlap segment (4-conn, Alg. 1 l.14-18 / l.27-29 at run
-// granularity) plus, for 8-conn, the diagonal run contacts NE / NW that do not
-// overlap (reading R2/R10).  Out-of-tile neighbours count as background.
-template <int TY, int CONN, typename F>
-__device__ __forceinline__ void for_each_row_event(const TileSmem<TY>& sm, int r, int lane, F f) {
-    const uint32_t cur = sm.wd[r][lane].m, up = sm.wd[r - 1][lane].m;
-    uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
-    uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
-    if (lane == 0) { curL = 0; upL = 0; }
-    if (lane == 31) { curR = 0; upR = 0; }
-    const uint32_t o = cur & up, oL = curL & upL;
-    uint32_t ev = o & ~((o << 1) | (oL >> 31));  // overlap-segment starts
-    const int rb = r * kTileW, ub = (r - 1) * kTileW, xb = lane << 5;
-    const Word* wc = sm.wd[r];
-    const Word* wu = sm.wd[r - 1];
-    while (ev) {
-        const int x = xb + __ffs(ev) - 1;
-        ev &= ev - 1;
-        f(rb + run_start_x(wc, x), ub + run_start_x(wu, x));
-    }
-    if (CONN == 8) {
-        const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
-        const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
-        uint32_t ne = cur & ~cur_n & ~up & up_n;  // upper run starts at x+1
-        uint32_t nw = cur & ~cur_p & ~up & up_p;  // current run starts at x, upper ends at x-1
-        while (ne) {
-            const int x = xb + __ffs(ne) - 1;
-            ne &= ne - 1;
-            f(rb + run_start_x(wc, x), ub + x + 1);
-        }
-        while (nw) {
-            const int x = xb + __ffs(nw) - 1;
-            nw &= nw - 1;
-            f(rb + x, ub + run_start_x(wu, x - 1));
-        }
-    }
-}
-
 // Calls f(l) for every run start l of tile row r held by this lane.
 template <int TY, typename F>
 __device__ __forceinline__ void for_each_run_start(const TileSmem<TY>& sm, int r, int lane, F f) {
@@ -320,115 +309,170 @@ __device__ __forceinline__ void for_each_run_start(const TileSmem<TY>& sm, int r
     }
 }
 
-// Local merge of one tile whose masks / runs / P are initialised in smem.
-// Coarse labeling: the row scan + row unification of Alg. 1 (l.9-13, l.19-24
-// in the row direction) is exact here -- every pixel's provisional label is
-// its run start, the lowest equivalent label of its row segment.
-// COARSE_COLUMN additionally performs the column scan (l.14-18) at run
-// granularity before the local UF:
-//  L2 every run takes as parent the leftmost run of the row above it touches
-//     (atomicMin of upper run starts: lower indices, so P[l] <= l throughout);
-//  L3 row-column unification: every run walks its parent chain to its end and
-//     records it (chains bounded by TY);
-//  L4 local UF (Alg. 1 l.25-33) on the remaining adjacencies, most of which are
-//     dismissed by one comparison of the coarse labels.
-// Without COARSE_COLUMN, L4 runs directly on the run adjacencies (measured
-// faster on B200).  L5 flattens: every run start
-// points at its local root.
-template <int TY, int CONN, bool COARSE_COLUMN = false>
-__device__ __forceinline__ void tile_local_uf(TileSmem<TY>& sm, int warp, int lane) {
-    __syncthreads();
-    volatile int32_t* V = sm.P;
-    if (COARSE_COLUMN) {
-        for (int r = warp + 1; r < TY; r += kWarps)
-            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) { atomicMin(&sm.P[cs >> 1], us); });
-        __syncthreads();
-        for (int r = warp + 1; r < TY; r += kWarps)
-            for_each_run_start<TY>(sm, r, lane, [&](int l) {
-                int t = l, p = V[l >> 1];
-                while (p != t) {
-                    t = p;
-                    p = V[t >> 1];
-                    V[l >> 1] = t;
-                }
-            });
-        __syncthreads();
-        for (int r = warp + 1; r < TY; r += kWarps)
-            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) {
-                if (V[cs >> 1] != V[us >> 1]) union_s(sm.P, cs, us);
-            });
-    } else {
-        for (int r = warp + 1; r < TY; r += kWarps)
-            for_each_row_event<TY, CONN>(sm, r, lane, [&](int cs, int us) { union_s(sm.P, cs, us); });
-    }
-    __syncthreads();
-    for (int r = warp; r < TY; r += kWarps)
-        for_each_run_start<TY>(sm, r, lane, [&](int l) { V[l >> 1] = find_s_ro(sm.P, l); });
-    __syncthreads();
-}
-
-// Edge enumeration shared by K1 (write G) and K3 (flag roots): calls f(l, ls)
-// for every foreground tile-edge item, l = tile-local index of the edge pixel,
-// ls = tile-local index of the run start owning it (P[ls>>1] is its root after
-// flattening).  Items: top-row run starts (if a tile is above), bottom-row run
-// starts (if a tile is below), left-column pixels (if a tile is left),
-// right-column pixels (if a tile is right).  K1 and K3 enumerate the same set,
-// so K3 reads G only where K1 wrote it.
-template <int TY, typename F>
-__device__ __forceinline__ void for_each_edge_item(const TileSmem<TY>& sm, const Geom& g,
-                                                   const TileId& id, int warp, int lane, F f) {
-    const int rows = min(TY, g.H - id.y0);
-    if (warp == 0 && id.y0 > 0) {
-        uint32_t t = sm.wd[0][lane].s;
-        while (t) {
-            const int bit = __ffs(t) - 1;
-            t &= t - 1;
-            const int l = (lane << 5) + bit;
-            f(l, l);
-        }
-    } else if (warp == 1 && id.y0 + TY < g.H) {
-        uint32_t t = sm.wd[TY - 1][lane].s;
-        while (t) {
-            const int bit = __ffs(t) - 1;
-            t &= t - 1;
-            const int l = (TY - 1) * kTileW + (lane << 5) + bit;
-            f(l, l);
-        }
-    } else if (warp == 2 && id.x0 > 0) {
-        for (int r = lane; r < rows; r += 32)
-            if (sm.wd[r][0].m & 1u) f(r * kTileW, r * kTileW);
-    } else if (warp == 3 && id.x0 + kTileW < g.W) {
-        for (int r = lane; r < rows; r += 32)
-            if (sm.wd[r][kWords - 1].m >> 31)
-                f(r * kTileW + kTileW - 1, r * kTileW + run_start_x(sm.wd[r], kTileW - 1));
-    }
-}
-
 // =========================================================== K1: local merge
-template <int TY, int CONN, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restrict__ img, Geom g,
-                                                          uint32_t* __restrict__ bits,
-                                                          int32_t* __restrict__ G,
-                                                          uint16_t* __restrict__ R) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileId id = decode_tile<TY>(g, blockIdx.x);
+// The tile's foreground is first turned into compact run lists (one entry per
+// row run, in raster order of the run starts) so every later step -- local UF,
+// flatten, edge output, per-run records -- runs one thread per run with all
+// lanes busy, instead of looping over the set bits of each lane's mask word.
+//
+// Coarse labeling (Alg. 1 l.9-24): the row scan + row-column unification in
+// the row direction is exact here -- every pixel's provisional label is its
+// run, the lowest equivalent label of its row segment.
+// Local UF (Alg. 1 l.25-33): each run of row r >= 1 finds the runs of row r-1
+// it touches in O(1) from the masks (they are a contiguous index range of the
+// sorted upper run list) and min-unions with each (8-conn widens the contact
+// interval by one pixel on both sides: the NW / NE diagonals, reading R2/R10).
+// Persistent: each block walks tiles t = blockIdx.x, +gridDim.x, ...; the
+// 128-bit image loads of the NEXT tile are issued into registers before the
+// current tile is processed, so HBM reads overlap the shared-memory work.
+
+// One 32-px mask word of a K1 tile row.
+struct __align__(16) WordE {
+    uint32_t m;    // foreground mask
+    uint32_t s;    // run-start mask (tile-local runs)
+    uint32_t e;    // run-end mask
+    int32_t pad;   // number of run starts in the row before this word
+};
+
+template <int TY>
+struct K1Smem {
+    WordE wd[TY][kWords];
+    uint16_t rs[TY * kTileW / 2];  // run k: start x | row << 10
+    uint16_t re[TY * kTileW / 2];  // run k: end x
+    int32_t P[TY * kTileW / 2];    // parent over tile run ids (min-root forest)
+    uint32_t flag[TY * kTileW / 64];  // run k is a root whose component touches a tile edge
+    int32_t fpre[TY * kTileW / 64];   // exclusive prefix of popc(flag[])
+    int32_t wsum[kWarps];
+    int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
+    int32_t rcnt[TY];              // runs per row
+    int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
+};
+
+// find / merge of §2.1.3 over tile run ids.
+__device__ __forceinline__ int find_r(int32_t* P, int a) {
+    volatile int32_t* V = P;
+    int p = V[a];
+    CCL_LOOP_GUARD(fr);
+    while (p != a) {
+        CCL_LOOP_TICK(fr);
+        const int gp = V[p];
+        if (gp != p) V[a] = gp;  // path halving: re-point at an ancestor
+        a = p;
+        p = gp;
+    }
+    return a;
+}
+
+__device__ __forceinline__ int find_r_ro(const int32_t* P, int a) {
+    const volatile int32_t* V = P;
+    int p = V[a];
+    CCL_LOOP_GUARD(fro);
+    while (p != a) {
+        CCL_LOOP_TICK(fro);
+        a = p;
+        p = V[a];
+    }
+    return a;
+}
+
+// Lock-free minimum-root union (reading R11): the larger root is re-pointed at
+// the smaller with atomicMin; if someone else re-linked it first, retry with
+// the value it was linked to.
+__device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
+    while (true) {
+        a = find_r(P, a);
+        b = find_r(P, b);
+        if (a == b) return;
+        if (a < b) { int t = a; a = b; b = t; }
+        const int old = atomicMin(&P[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// Profiling builds only (DBG bit 2): per-tile phase timestamps.
+__device__ unsigned long long* g_k1_stamps = nullptr;
+__device__ unsigned long long* g_k3_stamps = nullptr;
+__device__ __forceinline__ void k1_stamp(unsigned t, int k) {
+    if (g_k1_stamps) g_k1_stamps[size_t(t) * 8 + k] = clock64();
+}
+__device__ __forceinline__ void k3_stamp(unsigned t, int k) {
+    if (g_k3_stamps) g_k3_stamps[size_t(t) * 8 + k] = clock64();
+}
+
+template <int TY>
+struct ImgRegs {
+    uint4 v[TY / kWarps][2];
+};
+
+template <int TY>
+__host__ __device__ constexpr bool k1_prefetches() { return TY <= 16; }
+
+template <int TY>
+__device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, unsigned t, int warp,
+                                            int lane, ImgRegs<TY>& pf) {
+    const TileId id = decode_tile<TY>(g, t);
+    const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
+#pragma unroll
+    for (int i = 0; i < TY / kWarps; ++i) {
+        const int y = id.y0 + warp + i * kWarps;
+        pf.v[i][0] = make_uint4(0, 0, 0, 0);
+        pf.v[i][1] = make_uint4(0, 0, 0, 0);
+        if (y < g.H) {
+            const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
+            if (id.x0 + 16 * lane < g.W) pf.v[i][0] = ld_stream_u4(row + 16 * lane);
+            if (id.x0 + 512 + 16 * lane < g.W) pf.v[i][1] = ld_stream_u4(row + 512 + 16 * lane);
+        }
+    }
+}
+
+// Row r's mask word for this lane -> start / end masks, row-local run offsets.
+template <int TY>
+__device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uint32_t m) {
+    uint32_t pm = __shfl_up_sync(kFull, m, 1), nm = __shfl_down_sync(kFull, m, 1);
+    if (lane == 0) pm = 0;
+    if (lane == 31) nm = 0;
+    const uint32_t s = m & ~((m << 1) | (pm >> 31));
+    const uint32_t e = m & ~((m >> 1) | (nm << 31));
+    const int n = __popc(s);
+    int incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+    }
+    sm.wd[r][lane] = WordE{m, s, e, incl - n};
+    if (lane == 31) sm.rcnt[r] = incl;
+}
+
+template <int TY, int CONN, bool VEC, int DBG = 0>
+__device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
+                                        const ImgRegs<TY>& cur, uint32_t* bits, int32_t* G,
+                                        uint32_t* R, int32_t* E, int warp, int lane) {
+    const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
+    const int tid = threadIdx.x;
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 0);
 
-    for (int i = threadIdx.x; i < TY * kTileW / 64; i += kThreads) sm.flag[i] = 0;
-    // Alg. 1 l.3-8: load the tile (out-of-image pixels read as background, R5)
-    for (int r = warp; r < TY; r += kWarps) {
+    // Alg. 1 l.3-8: the tile's pixels -> foreground masks (out-of-image pixels
+    // read as background, R5)
+#pragma unroll
+    for (int i = 0; i < TY / kWarps; ++i) {
+        const int r = warp + i * kWarps;
         const int y = id.y0 + r;
         uint32_t m = 0;
         if (VEC) {
-            uint32_t h0 = 0, h1 = 0;
-            if (y < g.H) {
-                const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
-                if (id.x0 + 16 * lane < g.W) h0 = nz16(ld_stream_u4(row + 16 * lane));
-                if (id.x0 + 512 + 16 * lane < g.W) h1 = nz16(ld_stream_u4(row + 512 + 16 * lane));
+            uint4 v0 = cur.v[i][0], v1 = cur.v[i][1];
+            if (!k1_prefetches<TY>()) {  // tall tiles: load in place (register budget)
+                v0 = v1 = make_uint4(0, 0, 0, 0);
+                if (y < g.H) {
+                    const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
+                    if (id.x0 + 16 * lane < g.W) v0 = ld_stream_u4(row + 16 * lane);
+                    if (id.x0 + 512 + 16 * lane < g.W) v1 = ld_stream_u4(row + 512 + 16 * lane);
+                }
             }
+            const uint32_t h0 = nz16(v0), h1 = nz16(v1);
             const int src = (2 * lane) & 31;
             const uint32_t a0 = __shfl_sync(kFull, h0, src), a1 = __shfl_sync(kFull, h0, src + 1);
             const uint32_t b0 = __shfl_sync(kFull, h1, src), b1 = __shfl_sync(kFull, h1, src + 1);
@@ -445,54 +489,231 @@ __global__ void __launch_bounds__(kThreads) k_local_merge(const uint8_t* __restr
         }
         const int wg = id.tx * kWords + lane;
         if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
-        tile_row_init<TY, true>(sm, r, lane, m);
+        k1_row_init<TY>(sm, r, lane, m);
     }
-    tile_local_uf<TY, CONN>(sm, warp, lane);
-
-    // Alg. 1 l.34-39 for tile-edge items only: G[g(l)] = g(root), G[g(root)] = g(root);
-    // and flag the roots whose component touches a tile edge
-    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
-    const int W = g.W, x0 = id.x0, y0 = id.y0;
-    for_each_edge_item<TY>(sm, g, id, warp, lane, [&](int l, int ls) {
-        const int root = sm.P[ls >> 1];
-        const int gl = (y0 + (l >> 10)) * W + x0 + (l & 1023);
-        const int gr = (y0 + (root >> 10)) * W + x0 + (root & 1023);
-        Gb[gl] = gr;
-        Gb[gr] = gr;
-        atomicOr(&sm.flag[root >> 6], 1u << ((root >> 1) & 31));
-    });
+    for (int i = tid; i < TY * kTileW / 64; i += kThreads) sm.flag[i] = 0;
+    if (tid < TY) sm.lc[tid] = -1;
+    else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
     __syncthreads();
-    // per-run records for K3 (local root + edge flag), runs in raster order
-    uint16_t* Rt = R + size_t(blockIdx.x) * runs_per_tile_cap<TY>();
-    for (int r = warp; r < TY; r += kWarps) {
-        const int k0 = row_run_base<TY>(sm, r, lane) + sm.wd[r][lane].pad;
-        int j = 0;
-        for_each_run_start<TY>(sm, r, lane, [&](int l) {
-            const int root = sm.P[l >> 1];
-            const int e = (sm.flag[root >> 6] >> ((root >> 1) & 31)) & 1u;
-            Rt[k0 + j++] = uint16_t(root | (e ? kRunEdgeBit : 0));
-        });
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
+
+    // run lists: rs / re in raster order of the starts; P[k] = k
+    int total;
+    {
+        int v = lane < TY ? sm.rcnt[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(kFull, v, d);
+            if (lane >= d) v += u;
+        }
+        total = __shfl_sync(kFull, v, TY - 1);
+        if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
+        if (warp == 0 && lane == 0) sm.rbase[0] = 0;
+        for (int i = 0; i < TY / kWarps; ++i) {
+            const int r = warp + i * kWarps;
+            const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
+            const WordE w = sm.wd[r][lane];
+            const int xb = lane << 5;
+            int k = rb + w.pad;
+            uint32_t bits_ = w.s;
+            while (bits_) {
+                const int bit = __ffs(bits_) - 1;
+                bits_ &= bits_ - 1;
+                sm.rs[k++] = uint16_t((xb + bit) | (r << 10));
+            }
+            k = rb + w.pad - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
+            bits_ = w.e;
+            while (bits_) {
+                const int bit = __ffs(bits_) - 1;
+                bits_ &= bits_ - 1;
+                sm.re[k++] = uint16_t(xb + bit);
+            }
+        }
+    }
+    for (int k = tid; k < total; k += kThreads) sm.P[k] = k;
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
+    if (DBG & 1) {
+        __syncthreads();
+        return;
+    }
+
+    // local UF.  The adjacencies between two rows form a monotone staircase of
+    // run pairs; every pair is (k, first upper neighbour of k) or (first lower
+    // neighbour of j, j) -- if j is the 2nd+ upper neighbour of k, j starts
+    // right of k's start, so it cannot reach k-1.  Each run therefore does at
+    // most two unions, found in O(1) from the masks: no fan-in serialisation.
+    constexpr int D = CONN == 8 ? 1 : 0;
+    for (int k = tid; k < total; k += kThreads) {
+        const int rsk = sm.rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        if (r > 0) {  // first run of row r-1 touching [p, q]
+            const WordE u = sm.wd[r - 1][p >> 5];
+            const int open = (u.m & 1u) && !(u.s & 1u);
+            const int j = sm.rbase[r - 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            if (j < sm.rbase[r] && (sm.rs[j] & 1023) <= q) union_r(sm.P, k, j);
+        }
+        if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
+            const WordE u = sm.wd[r + 1][p >> 5];
+            const int open = (u.m & 1u) && !(u.s & 1u);
+            const int j = sm.rbase[r + 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            if (j < sm.rbase[r + 2] && (sm.rs[j] & 1023) <= q) union_r(sm.P, j, k);
+        }
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
+    for (int k = tid; k < total; k += kThreads) sm.P[k] = find_r_ro(sm.P, k);
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
+    if (DBG & 2) {
+        __syncthreads();
+        return;
+    }
+
+    // Alg. 1 l.34-39 for tile-edge items only (reading R7 for the index
+    // conversion): flag the roots of top / bottom row runs and of left / right
+    // column pixels; record the column pixels' roots for the boundary analysis.
+    const int W = g.W, x0 = id.x0, y0 = id.y0;
+    const bool top = y0 > 0, bottom = y0 + TY < g.H, left = x0 > 0, right = x0 + kTileW < W;
+    for (int k = tid; k < total; k += kThreads) {
+        const int rsk = sm.rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
+        const bool hrow = (r == 0 && top) || (r == TY - 1 && bottom);
+        const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
+        if (hrow || lc || rc) {
+            const int root = sm.P[k];
+            atomicOr(&sm.flag[root >> 5], 1u << (root & 31));
+            if (lc || rc) {
+                const int rr = sm.rs[root];
+                const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+                if (lc) sm.lc[r] = gr;
+                if (rc) sm.rc[r] = gr;
+            }
+        }
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
+    // edge-root list order: exclusive prefix of the flag bits (raster order of
+    // the roots, so the lists are deterministic)
+    {
+        constexpr int NW = TY * kTileW / 64;   // flag words
+        constexpr int PER = (NW + kThreads - 1) / kThreads;
+        int loc[PER], sum = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int w = tid * PER + i;
+            loc[i] = w < NW ? __popc(sm.flag[w]) : 0;
+            sum += loc[i];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += u;
+        }
+        if (lane == 31) sm.wsum[warp] = incl;
+        __syncthreads();
+        int wb = 0;
+        for (int i = 0; i < warp; ++i) wb += sm.wsum[i];
+        int run = wb + incl - sum;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int w = tid * PER + i;
+            if (w < NW) sm.fpre[w] = run;
+            run += loc[i];
+        }
+        if (tid == kThreads - 1) E[size_t(t) * kEdgeCap] = wb + incl;  // list length
+    }
+    __syncthreads();
+    // edge block header + column roots, per-run records for K3, the edge-root
+    // list, and the global parent entries G[root] = root of the edge roots.
+    // Those are written as whole 32-byte sectors (identity for the 8 pixels:
+    // no other entry of G is ever read) so the boundary analysis' atomics and
+    // loads hit fully valid L2 sectors instead of filling from DRAM.
+    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
+    int32_t* Eh = E + size_t(t) * kEdgeCap;
+    if (tid == 0) Eh[1] = sm.rbase[TY - 1];
+    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
+    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
+    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+    int32_t* Et = Eh + kEdgeList;
+    for (int k = tid; k < total; k += kThreads) {
+        const int root = sm.P[k];
+        const int rr = sm.rs[root];  // row*1024 + x of the root run's start
+        const uint32_t fw = sm.flag[root >> 5];
+        uint32_t rec = uint32_t(rr);
+        if ((fw >> (root & 31)) & 1u) {
+            const int idx = sm.fpre[root >> 5] + __popc(fw & ((1u << (root & 31)) - 1u));
+            rec |= uint32_t(idx + 1) << 16;
+            if (k == root) {
+                const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+                Et[idx] = gr;
+                if ((g.npx & 7) == 0) {
+                    // whole sector, identity: harmless for the 7 neighbours
+                    // (every root entry is still its own index during K1, all
+                    // other entries are never read); images are sector-aligned
+                    const int base = gr & ~7;
+                    int4* sec = reinterpret_cast<int4*>(Gb + base);
+                    sec[0] = make_int4(base, base + 1, base + 2, base + 3);
+                    sec[1] = make_int4(base + 4, base + 5, base + 6, base + 7);
+                } else {
+                    Gb[gr] = gr;
+                }
+            }
+        }
+        Rt[k] = rec;
+    }
+    __syncthreads();  // smem is reused by the next tile
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
+}
+
+template <int TY, int CONN, bool VEC, int DBG = 0>
+__global__ void __launch_bounds__(kThreads, 3) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+                                                             uint32_t* __restrict__ bits,
+                                                             int32_t* __restrict__ G,
+                                                             uint32_t* __restrict__ R,
+                                                             int32_t* __restrict__ E,
+                                                             unsigned ntiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K1Smem<TY>& sm = *reinterpret_cast<K1Smem<TY>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned t = blockIdx.x;
+    if (t >= ntiles) return;
+    constexpr bool PF = VEC && k1_prefetches<TY>();
+    // two register sets used alternately (no copies): a holds tile t while b
+    // receives tile t + gridDim.x, then the roles swap
+    ImgRegs<TY> a, b;
+    if (PF) k1_prefetch<TY>(img, g, t, warp, lane, a);
+    while (true) {
+        if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, b);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, bits, G, R, E, warp, lane);
+        t += gridDim.x;
+        if (t >= ntiles) break;
+        if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, a);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, b, bits, G, R, E, warp, lane);
+        t += gridDim.x;
+        if (t >= ntiles) break;
     }
 }
 
 // ============================================================ K2: boundary
-// Warp-cooperative union of a batch of (run start / edge pixel) index pairs:
-// each lane holds at most one pair (ia, ib) (ia < 0: none).  Step 1 reads the
-// local roots G[ia], G[ib] written by K1 (one independent load per lane);
-// step 2 drops pairs already seen in this warp (identical root pairs are
-// common: two large components meet at many places along a tile edge) so only
-// one lane per distinct pair runs the global min-union.  This keeps the hot
-// root of a giant component from being read once per crossing edge.
-__device__ __forceinline__ void warp_union_pairs(int32_t* G, int ia, int ib, unsigned long long& last,
+// Boundary analysis (Alg. 2, §2.2): min-union of the local roots on the two
+// sides of every foreground edge that crosses a tile boundary (reading R9 /
+// R10).  The local roots come from K1's compact outputs -- the per-run records
+// of the tile rows next to a horizontal boundary and the column-root lists of
+// the tiles next to a vertical boundary -- so the only scattered accesses left
+// are the union walks over the roots' parent entries in G.
+//
+// Warp-cooperative union of a batch of root pairs: each lane holds at most one
+// pair (a, b) (a < 0: none).  Pairs already seen in this warp are dropped
+// (identical root pairs are common: two large components meet at many places
+// along a tile edge) so only one lane per distinct pair runs the union.
+__device__ __forceinline__ void warp_union_pairs(int32_t* G, int a, int b, unsigned long long& last,
                                                  int img) {
-    int a = -1, b = -1;
-    if (ia >= 0) {
-        a = ld_volatile(G + ia);
-        b = ld_volatile(G + ib);
-        if (a > b) { int t = a; a = b; b = t; }
-    }
+    if (a > b) { int t = a; a = b; b = t; }
     const unsigned long long key =
-        (ia >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
+        (a >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
     // pairs are only equal within one image (G values are image-local indices)
     const unsigned grp = __match_any_sync(kFull, key) & __match_any_sync(kFull, img);
     const int lane = threadIdx.x & 31;
@@ -500,16 +721,26 @@ __device__ __forceinline__ void warp_union_pairs(int32_t* G, int ia, int ib, uns
     if (key != ~0ull) last = key;
 }
 
+// image-local raster index of a K1 run record's root (tile origin x0, y0)
+__device__ __forceinline__ int rec_root(uint32_t rec, int W, int x0, int y0) {
+    const int rr = int(rec & 0x7FFFu);
+    return (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+}
+
 // Horizontal tile edges: one warp per (image, band >= 1, tile column); vertical
 // tile edges: one thread per (image, tile column boundary >= 1, row).
-template <int TY, int CONN>
+template <int TY, int CONN, int DBG = 0>
 __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
+                                                  const uint32_t* __restrict__ R,
+                                                  const int32_t* __restrict__ E,
                                                   int32_t* __restrict__ G, long long n_h,
                                                   long long blocks_h) {
     __shared__ Word s_w[8][2][kWords];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long last = ~0ull;
+    constexpr int RCAP = runs_per_tile_cap<TY>();
     if (blockIdx.x < blocks_h) {
+        if (DBG & 2) return;  // profiling: skip horizontal edges
         const long long task = (long long)blockIdx.x * 8 + warp;
         if (task >= n_h) return;  // whole warp exits together
         long long t = task;
@@ -518,8 +749,14 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         const int band = 1 + int(t % (g.tiles_y - 1));
         const int b = int(t / (g.tiles_y - 1));
         const int x0 = tx * kTileW, y0 = band * TY;
+        const size_t t_lo = (size_t(b) * g.tiles_y + band) * g.tiles_x + tx;  // tile below the edge
+        const size_t t_up = t_lo - g.tiles_x;                                 // tile above
         const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
         int32_t* Gb = G + size_t(b) * size_t(g.npx);
+        const uint32_t* Rlo = R + t_lo * RCAP;                        // row 0 runs start at id 0
+        const int up_base = E[t_up * kEdgeCap + 1];
+        CCL_ASSERT(up_base >= 0 && up_base < RCAP);
+        const uint32_t* Rup = R + t_up * RCAP + up_base;  // last row's runs
         const int wg = tx * kWords + lane;
         const uint32_t cur = wg < g.WW ? bm[size_t(y0) * g.WW + wg] : 0u;
         const uint32_t up = wg < g.WW ? bm[size_t(y0 - 1) * g.WW + wg] : 0u;
@@ -527,8 +764,15 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         int cc, cu;
         row_runs(cur, lane, sc, cc);
         row_runs(up, lane, su, cu);
-        s_w[warp][0][lane] = Word{cur, sc, cc, 0};
-        s_w[warp][1][lane] = Word{up, su, cu, 0};
+        // row-local run index of the first start in each word (prefix of popc)
+        int ic = __popc(sc), iu = __popc(su);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int a = __shfl_up_sync(kFull, ic, d), c = __shfl_up_sync(kFull, iu, d);
+            if (lane >= d) { ic += a; iu += c; }
+        }
+        s_w[warp][0][lane] = Word{cur, sc, cc, ic - __popc(sc)};
+        s_w[warp][1][lane] = Word{up, su, cu, iu - __popc(su)};
         __syncwarp();
         uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
         uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
@@ -546,36 +790,47 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
             if (lane == 0 && tx > 0 && (cur & 1u)) cnw = bm[size_t(y0 - 1) * g.WW + wg - 1] >> 31;
             if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = bm[size_t(y0 - 1) * g.WW + wg + 1] & 1u;
         }
-        const int gc = y0 * g.W + x0, gu = (y0 - 1) * g.W + x0, xb = lane << 5;
+        // run index (within its row) of the run containing foreground pixel x:
+        // (number of run starts at positions <= x) - 1
+        auto run_idx = [&](int row, int x) {
+            CCL_ASSERT(x >= 0 && x < kTileW);
+            const Word& w = s_w[warp][row][x >> 5];
+            const int i = w.pad + __popc(w.s & (kFull >> (31 - (x & 31)))) - 1;
+            CCL_ASSERT(i >= 0 && i < kTileW / 2);
+            return i;
+        };
+        const int W = g.W;
         while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
-            int ia = -1, ib = -1;
+            int a = -1, c = -1;
             if (ev) {
-                const int x = xb + __ffs(ev) - 1;
+                const int x = (lane << 5) + __ffs(ev) - 1;
                 ev &= ev - 1;
-                ia = gc + run_start_x(s_w[warp][0], x);
-                ib = gu + run_start_x(s_w[warp][1], x);
+                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
+                c = rec_root(Rup[run_idx(1, x)], W, x0, y0 - TY);
             } else if (ne) {
-                const int x = xb + __ffs(ne) - 1;
+                const int x = (lane << 5) + __ffs(ne) - 1;
                 ne &= ne - 1;
-                ia = gc + run_start_x(s_w[warp][0], x);
-                ib = gu + x + 1;
+                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
+                c = rec_root(Rup[run_idx(1, x + 1)], W, x0, y0 - TY);
             } else if (nw) {
-                const int x = xb + __ffs(nw) - 1;
+                const int x = (lane << 5) + __ffs(nw) - 1;
                 nw &= nw - 1;
-                ia = gc + x;
-                ib = gu + run_start_x(s_w[warp][1], x - 1);
-            } else if (cnw) {
+                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
+                c = rec_root(Rup[run_idx(1, x - 1)], W, x0, y0 - TY);
+            } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
                 cnw = false;
-                ia = gc;            // (x0, y0)
-                ib = gu - 1;        // (x0-1, y0-1)
-            } else if (cne) {
+                a = E[t_lo * kEdgeCap + kEdgeLC];
+                c = E[(t_up - 1) * kEdgeCap + kEdgeRC + TY - 1];
+            } else if (cne) {  // (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
                 cne = false;
-                ia = gc + kTileW - 1;  // (x0+1023, y0)
-                ib = gu + kTileW;      // (x0+1024, y0-1)
+                a = E[t_lo * kEdgeCap + kEdgeRC];
+                c = E[(t_up + 1) * kEdgeCap + kEdgeLC + TY - 1];
             }
-            warp_union_pairs(Gb, ia, ib, last, 0);
+            CCL_ASSERT(a < 0 || (a < g.npx && c >= 0 && c < g.npx));
+            warp_union_pairs(Gb, a, c, last, 0);
         }
     } else {
+        if (DBG & 1) return;  // profiling: skip vertical edges
         const long long task = (long long)(blockIdx.x - blocks_h) * 256 + threadIdx.x;
         const int nbx = g.tiles_x - 1;
         const long long n_v = (long long)g.B * g.H * nbx;
@@ -585,26 +840,43 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         t /= g.H;
         const int bx = 1 + int(t % nbx);
         const int b = int(t / nbx);
-        const int x0 = bx * kTileW;
-        const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
+        const int band = y / TY, r = y - band * TY;
+        const size_t tr = (size_t(b) * g.tiles_y + band) * g.tiles_x + bx;  // tile right of the edge
+        const int32_t* Er = E + tr * kEdgeCap;
+        const int32_t* El = Er - kEdgeCap;                                 // tile left of the edge
         int32_t* Gb = G + size_t(b) * size_t(g.npx);
-        const int wl = bx * kWords - 1;
-        const size_t row = size_t(y) * g.WW;
-        bool L = false, R = false, Lu = false, Ru = false;
+        int L = -1, Rr = -1, Lu = -1, Ru = -1;
         if (valid) {
-            L = bm[row + wl] >> 31;
-            R = bm[row + wl + 1] & 1u;
-            if (CONN == 8 && (y % TY) != 0 && (L || R)) {
-                Lu = bm[row - g.WW + wl] >> 31;
-                Ru = bm[row - g.WW + wl + 1] & 1u;
+            L = El[kEdgeRC + r];   // root of (x0-1, y), or -1
+            Rr = Er[kEdgeLC + r];  // root of (x0, y), or -1
+            if (CONN == 8 && r > 0 && (L >= 0 || Rr >= 0)) {
+                Lu = El[kEdgeRC + r - 1];
+                Ru = Er[kEdgeLC + r - 1];
             }
         }
-        const int p = y * g.W + x0;
-        warp_union_pairs(Gb, (L && R) ? p - 1 : -1, p, last, b);              // W edge of (x0, y)
+        warp_union_pairs(Gb, (L >= 0 && Rr >= 0) ? L : -1, Rr, last, b);      // W edge of (x0, y)
         if (CONN == 8) {
-            warp_union_pairs(Gb, (R && Lu) ? p : -1, p - g.W - 1, last, b);   // NW of (x0, y)
-            warp_union_pairs(Gb, (L && Ru) ? p - 1 : -1, p - g.W, last, b);   // NE of (x0-1, y)
+            warp_union_pairs(Gb, (Rr >= 0 && Lu >= 0) ? Rr : -1, Lu, last, b);  // NW of (x0, y)
+            warp_union_pairs(Gb, (L >= 0 && Ru >= 0) ? L : -1, Ru, last, b);    // NE of (x0-1, y)
         }
+    }
+}
+
+// ------------------------------------------- K2 tail: resolve edge roots
+// Boundary analysis, last step: every edge-touching local root of every tile
+// is resolved to its global root (find) once, all in parallel,
+// and 1 + root is stored in the tile's F list, so K3 needs no pointer chasing.
+template <int TY>
+__global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restrict__ G,
+                                                 const int32_t* __restrict__ E,
+                                                 int32_t* __restrict__ F, unsigned ntiles) {
+    const int lane = threadIdx.x & 31;
+    const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
+    for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
+        const int32_t* Et = E + size_t(t) * kEdgeCap;
+        const int n = Et[0];
+        const int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
+        for (int i = lane; i < n; i += 32) F[size_t(t) * kEdgeCap + i] = find_g_ro(Gb, Et[kEdgeList + i]) + 1;
     }
 }
 
@@ -613,55 +885,69 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // starts only, no union-find) and take their local root from K1's per-run
 // records; roots whose component touches a tile edge are resolved through G
 // (find); then every pixel gets 1 + its global root, or 0.
-template <int TY, int CONN, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_link(Geom g, const uint32_t* __restrict__ bits,
-                                                   int32_t* __restrict__ G,
-                                                   const uint16_t* __restrict__ R,
-                                                   int32_t* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileId id = decode_tile<TY>(g, blockIdx.x);
+// Persistent like K1: the next tile's mask words and first kRunCache run
+// records are prefetched into registers while the current tile is written.
+template <int TY>
+struct LinkRegs {
+    uint32_t m[TY / kWarps];
+    uint4 runs;  // warps 0, 2: run records 4*i .. 4*i+3 (i = lane, 32 + lane)
+    int fin;     // warp 1: resolved label F[lane]
+};
+
+template <int TY>
+__device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t* R, const int32_t* F,
+                                            const Geom& g, unsigned t, int warp, int lane,
+                                            LinkRegs<TY>& pf) {
+    const TileId id = decode_tile<TY>(g, t);
     const uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
-    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
-    int32_t* ob = out + size_t(id.b) * size_t(g.npx);
-    const uint16_t* Rt = R + size_t(blockIdx.x) * runs_per_tile_cap<TY>();
-
-    for (int r = warp; r < TY; r += kWarps) {
-        const int y = id.y0 + r;
-        const int wg = id.tx * kWords + lane;
-        const uint32_t m = (y < g.H && wg < g.WW) ? __ldg(bm + size_t(y) * g.WW + wg) : 0u;
-        tile_row_init<TY, false>(sm, r, lane, m);
+    const int wg = id.tx * kWords + lane;
+#pragma unroll
+    for (int i = 0; i < TY / kWarps; ++i) {
+        const int y = id.y0 + warp + i * kWarps;
+        pf.m[i] = (y < g.H && wg < g.WW) ? __ldg(bm + size_t(y) * g.WW + wg) : 0u;
     }
-    __syncthreads();
+    if (warp == 0 || warp == 2)
+        pf.runs = __ldg(reinterpret_cast<const uint4*>(R + size_t(t) * runs_per_tile_cap<TY>()) + lane +
+                        (warp == 2 ? 32 : 0));
+    if (warp == 1) pf.fin = __ldg(F + size_t(t) * kEdgeCap + lane);
+}
 
-    // pass A: P[l] <- local root (untagged) for non-roots; roots get their
-    // tagged final label 1 + global root
+template <int TY, int CONN, bool VEC, int DBG = 0>
+__device__ __forceinline__ void k3_tile(TileSmem<TY>& sm, const Geom& g, unsigned t, const LinkRegs<TY>& cur,
+                                        const uint32_t* R, const int32_t* F, int32_t* out, int warp,
+                                        int lane) {
+    const TileId id = decode_tile<TY>(g, t);
+    int32_t* ob = out + size_t(id.b) * size_t(g.npx);
+    const uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+    const int32_t* Ft = F + size_t(t) * kEdgeCap;
+    if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 0);
+
+    if (warp == 0 || warp == 2) reinterpret_cast<uint4*>(sm.rc)[lane + (warp == 2 ? 32 : 0)] = cur.runs;
+    if (warp == 1) sm.fc[lane] = cur.fin;
+#pragma unroll
+    for (int i = 0; i < TY / kWarps; ++i) tile_row_init<TY, false>(sm, warp + i * kWarps, lane, cur.m[i]);
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 1);
+
+    // every run start gets its final label: 1 + the global root, which is the
+    // local root (from K1's record) unless the component touches a tile edge,
+    // then it is the boundary analysis' resolved label
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     for (int r = warp; r < TY; r += kWarps) {
         const int k0 = row_run_base<TY>(sm, r, lane) + sm.wd[r][lane].pad;
         int j = 0;
         for_each_run_start<TY>(sm, r, lane, [&](int l) {
-            const int v = __ldg(Rt + k0 + j++);
-            const int root = v & (kRunEdgeBit - 1);
-            if (root == l) {
-                int gr = (y0 + r) * W + x0 + (l & 1023);
-                if (v & kRunEdgeBit) gr = find_g(Gb, gr);
-                sm.P[l >> 1] = (gr + 1) | kTag;
-            } else {
-                sm.P[l >> 1] = root;
-            }
+            const int k = k0 + j++;
+            const uint32_t v = k < kRunCache ? sm.rc[k] : __ldg(Rt + k);
+            const int e = int(v >> 16);  // 1 + edge-list index, or 0
+            const int rr = int(v & 0x7FFFu);
+            int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1;
+            if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
+            sm.P[l >> 1] = lab | kTag;
         });
     }
     __syncthreads();
-    // pass B: non-root run starts take their root's tagged label
-    for (int r = warp; r < TY; r += kWarps)
-        for_each_run_start<TY>(sm, r, lane, [&](int l) {
-            const int p = sm.P[l >> 1];
-            if (p >= 0) sm.P[l >> 1] = sm.P[p >> 1];
-        });
-    __syncthreads();
-
+    if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 2);
     // stream the labels; every run-start entry of P now holds its tagged label
     for (int r = warp; r < TY; r += kWarps) {
         const int y = y0 + r;
@@ -680,20 +966,20 @@ __global__ void __launch_bounds__(kThreads) k_link(Geom g, const uint32_t* __res
                 int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
                 if (fgn) {
                     const uint32_t stn = (wd.s >> sh) & 0xFu;
-                    int cur = 0;
+                    int c = 0;
                     if (fgn & 1u) {
                         const uint32_t below = wd.s & (kFull >> (31 - sh));
                         const int st = below ? ((w << 5) + 31 - __clz(below)) : wd.c;
-                        cur = sm.P[(rb + st) >> 1];
+                        c = sm.P[(rb + st) >> 1];
                     }
                     const int pb = (rb + x) >> 1;  // P index of pixel x+1 / x+2 / x+3 starts
-                    v0 = cur;
-                    if (stn & 2u) cur = sm.P[pb];          // start at x+1: (rb+x+1)>>1 == pb
-                    v1 = cur;
-                    if (stn & 4u) cur = sm.P[pb + 1];      // start at x+2
-                    v2 = cur;
-                    if (stn & 8u) cur = sm.P[pb + 1];      // start at x+3: (rb+x+3)>>1 == pb+1
-                    v3 = cur;
+                    v0 = c;
+                    if (stn & 2u) c = sm.P[pb];          // start at x+1: (rb+x+1)>>1 == pb
+                    v1 = c;
+                    if (stn & 4u) c = sm.P[pb + 1];      // start at x+2
+                    v2 = c;
+                    if (stn & 8u) c = sm.P[pb + 1];      // start at x+3: (rb+x+3)>>1 == pb+1
+                    v3 = c;
                     v0 = (fgn & 1u) ? (v0 & 0x7FFFFFFF) : 0;
                     v1 = (fgn & 2u) ? (v1 & 0x7FFFFFFF) : 0;
                     v2 = (fgn & 4u) ? (v2 & 0x7FFFFFFF) : 0;
@@ -715,6 +1001,32 @@ __global__ void __launch_bounds__(kThreads) k_link(Geom g, const uint32_t* __res
                 }
             }
         }
+    }
+    __syncthreads();  // smem is reused by the next tile
+    if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 3);
+}
+
+template <int TY, int CONN, bool VEC, int DBG = 0>
+__global__ void __launch_bounds__(kThreads, 4) k_link(Geom g, const uint32_t* __restrict__ bits,
+                                                      const uint32_t* __restrict__ R,
+                                                      const int32_t* __restrict__ F,
+                                                      int32_t* __restrict__ out, unsigned ntiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned t = blockIdx.x;
+    if (t >= ntiles) return;
+    LinkRegs<TY> a, b;
+    k3_prefetch<TY>(bits, R, F, g, t, warp, lane, a);
+    while (true) {
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, b);
+        k3_tile<TY, CONN, VEC, DBG>(sm, g, t, a, R, F, out, warp, lane);
+        t += gridDim.x;
+        if (t >= ntiles) break;
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, a);
+        k3_tile<TY, CONN, VEC, DBG>(sm, g, t, b, R, F, out, warp, lane);
+        t += gridDim.x;
+        if (t >= ntiles) break;
     }
 }
 

@@ -1,0 +1,211 @@
+// tools/k1_phases.cu -- profiling harness (not part of libccl.so): times the
+// K1 local-merge kernel with phases disabled (DBG template bits) and the HBM
+// read / write floors on the same image, to locate where K1/K3 time goes.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I include \
+//        tools/k1_phases.cu -o tools/k1_phases
+//   tools/k1_phases <raw uint8 image file> H W [conn]
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1708_08180_b200/csrc/ccl_kernels.cuh"
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) {                                                       \
+            fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+            exit(1);                                                                   \
+        }                                                                              \
+    } while (0)
+
+__global__ void read_floor(const uint4* p, size_t n, unsigned* sink) {
+    unsigned acc = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        uint4 v = ccl::ld_stream_u4(reinterpret_cast<const uint8_t*>(p + i));
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+__global__ void write_floor(int32_t* p, size_t n4) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x)
+        ccl::st_stream_i4(p + 4 * i, int(i), 0, 1, 2);
+}
+
+template <typename F>
+float timeit(F f, void* flush, size_t flush_bytes, int iters = 20) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float tot = 0;
+    for (int i = 0; i < iters + 3; ++i) {
+        CK(cudaMemsetAsync(flush, i, flush_bytes));
+        CK(cudaEventRecord(a));
+        f();
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (i >= 3) tot += ms;
+    }
+    CK(cudaGetLastError());
+    return 1000.f * tot / iters;
+}
+
+template <int TY, int CONN, int DBG>
+void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, int32_t* G, uint32_t* R,
+            int32_t* E, unsigned ntiles, int grid, void* flush, size_t fb) {
+    auto k = ccl::k_local_merge<TY, CONN, true, DBG>;
+    size_t smem = sizeof(ccl::K1Smem<TY>);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    float us = timeit([&] { k<<<grid, ccl::kThreads, smem>>>(img, g, bits, G, R, E, ntiles); }, flush, fb);
+    printf("%-34s grid %6d  %8.1f us\n", name, grid, us);
+}
+
+int main(int argc, char** argv) {
+    if (argc < 4) {
+        fprintf(stderr, "usage: %s image.raw H W [conn]\n", argv[0]);
+        return 2;
+    }
+    const int H = atoi(argv[2]), W = atoi(argv[3]);
+    const size_t n = size_t(H) * W;
+    std::vector<uint8_t> h(n);
+    FILE* f = fopen(argv[1], "rb");
+    if (!f || fread(h.data(), 1, n, f) != n) {
+        fprintf(stderr, "cannot read image\n");
+        return 2;
+    }
+    fclose(f);
+    uint8_t* img;
+    int32_t *G, *out;
+    uint32_t* bits;
+    uint32_t* R;
+    int32_t *E, *F;
+    void* flush;
+    const size_t fb = size_t(512) << 20;
+    CK(cudaMalloc(&img, n));
+    CK(cudaMalloc(&G, n * 4));
+    CK(cudaMalloc(&out, n * 4));
+    CK(cudaMalloc(&bits, n / 8 + 4096));
+    CK(cudaMalloc(&R, 2 * n + 65536));
+    CK(cudaMalloc(&E, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
+    CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
+    CK(cudaMalloc(&flush, fb));
+    unsigned* sink;
+    CK(cudaMalloc(&sink, 64));
+    CK(cudaMemcpy(img, h.data(), n, cudaMemcpyHostToDevice));
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+
+    float r = timeit([&] { read_floor<<<sms * 8, 256>>>(reinterpret_cast<const uint4*>(img), n / 16, sink); }, flush, fb);
+    printf("%-34s %8.1f us  %7.1f GB/s\n", "read floor (image, 1 B/px)", r, n / r / 1e3);
+    float w = timeit([&] { write_floor<<<sms * 8, 256>>>(out, n / 4); }, flush, fb);
+    printf("%-34s %8.1f us  %7.1f GB/s\n", "write floor (labels, 4 B/px)", w, 4 * n / w / 1e3);
+
+    constexpr int TY = 16;
+    ccl::Geom g;
+    g.B = 1;
+    g.H = H;
+    g.W = W;
+    g.WW = (W + 31) / 32;
+    g.tiles_x = (W + 1023) / 1024;
+    g.tiles_y = (H + TY - 1) / TY;
+    g.npx = n;
+    g.nwords = size_t(H) * g.WW;
+    const unsigned ntiles = g.tiles_x * g.tiles_y;
+    g.div_tx = ccl::FastDiv(g.tiles_x);
+    g.div_ty = ccl::FastDiv(g.tiles_y);
+    for (int per_sm : {2, 3}) {
+        int grid = std::min<int>(ntiles, sms * per_sm);
+        char nm[64];
+        snprintf(nm, sizeof nm, "K1 load+convert+runs (DBG=3) x%d", per_sm);
+        run_k1<TY, 8, 3>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
+        snprintf(nm, sizeof nm, "K1 +local UF (DBG=2) x%d", per_sm);
+        run_k1<TY, 8, 2>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
+        snprintf(nm, sizeof nm, "K1 full (DBG=0) x%d", per_sm);
+        run_k1<TY, 8, 0>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
+    }
+    run_k1<TY, 8, 0>("K1 full, one block per tile", img, g, bits, G, R, E, ntiles, ntiles, flush, fb);
+
+    // per-phase clock64 stamps (DBG bit 2), persistent grid x3
+    unsigned long long* st;
+    CK(cudaMalloc(&st, size_t(ntiles) * 8 * 8));
+    CK(cudaMemset(st, 0, size_t(ntiles) * 8 * 8));
+    CK(cudaMemcpyToSymbol(ccl::g_k1_stamps, &st, sizeof(st)));
+    run_k1<TY, 8, 4>("K1 full + stamps x3", img, g, bits, G, R, E, ntiles, std::min<int>(ntiles, sms * 3), flush, fb);
+    std::vector<unsigned long long> hs(size_t(ntiles) * 8);
+    CK(cudaMemcpy(hs.data(), st, hs.size() * 8, cudaMemcpyDeviceToHost));
+    const char* names[6] = {"convert+row init", "run lists", "union", "flatten", "edges+G", "run records"};
+    double acc[6] = {0};
+    for (unsigned t = 0; t < ntiles; ++t)
+        for (int k = 0; k < 6; ++k) acc[k] += double(hs[t * 8 + k + 1] - hs[t * 8 + k]);
+    double tot = 0;
+    for (int k = 0; k < 6; ++k) tot += acc[k];
+    printf("per-tile phase cycles (mean over %u tiles):\n", ntiles);
+    for (int k = 0; k < 6; ++k) printf("  %-18s %8.0f  (%4.1f%%)\n", names[k], acc[k] / ntiles, 100 * acc[k] / tot);
+    printf("  %-18s %8.0f\n", "total", tot / ntiles);
+
+    // K2 variants (each preceded by K1, which resets the G entries K2 touches)
+    auto k1 = ccl::k_local_merge<TY, 8, true, 0>;
+    const int grid1 = std::min<int>(ntiles, sms * 3);
+    const size_t sm1 = sizeof(ccl::K1Smem<TY>);
+    const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)g.H * (g.tiles_x - 1);
+    const long long bh = (n_h + 7) / 8, bv = (n_v + 255) / 256;
+    auto time_k2 = [&](auto k2, const char* nm) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        float tot2 = 0;
+        for (int i = 0; i < 23; ++i) {
+            CK(cudaMemsetAsync(flush, i, fb));
+            k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
+            CK(cudaEventRecord(a));
+            k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            if (i >= 3) tot2 += ms;
+        }
+        printf("%-34s %8.1f us\n", nm, 1000.f * tot2 / 20);
+    };
+    time_k2(ccl::k_boundary<TY, 8, 0>, "K2 full");
+    time_k2(ccl::k_boundary<TY, 8, 1>, "K2 horizontal only");
+    time_k2(ccl::k_boundary<TY, 8, 2>, "K2 vertical only");
+    time_k2(ccl::k_boundary<TY, 8, 3>, "K2 empty (launch)");
+    {
+        k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
+        ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+        float us = timeit([&] { ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles); }, flush, fb);
+        printf("%-34s %8.1f us\n", "K2b resolve", us);
+    }
+
+    // K3 (after K1 + K2), with stamps
+    k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
+    ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+    ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
+    auto k3 = ccl::k_link<TY, 8, true, 0>;
+    auto k3s = ccl::k_link<TY, 8, true, 4>;
+    const size_t sm3 = sizeof(ccl::TileSmem<TY>);
+    CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+    CK(cudaFuncSetAttribute(k3s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+    for (int per_sm : {3, 4, 5}) {
+        const int grid3 = std::min<int>(ntiles, sms * per_sm);
+        float us = timeit([&] { k3<<<grid3, ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles); }, flush, fb);
+        printf("K3 x%d                              %8.1f us\n", per_sm, us);
+    }
+    unsigned long long* st3;
+    CK(cudaMalloc(&st3, size_t(ntiles) * 8 * 8));
+    CK(cudaMemcpyToSymbol(ccl::g_k3_stamps, &st3, sizeof(st3)));
+    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles); }, flush, fb);
+    printf("K3 + stamps x4                     %8.1f us\n", us3);
+    CK(cudaMemcpy(hs.data(), st3, hs.size() * 8, cudaMemcpyDeviceToHost));
+    const char* n3[3] = {"load+row init", "run labels", "write"};
+    double a3[3] = {0}, t3 = 0;
+    for (unsigned t = 0; t < ntiles; ++t)
+        for (int k = 0; k < 3; ++k) a3[k] += double(hs[t * 8 + k + 1] - hs[t * 8 + k]);
+    for (int k = 0; k < 3; ++k) t3 += a3[k];
+    for (int k = 0; k < 3; ++k) printf("  %-18s %8.0f  (%4.1f%%)\n", n3[k], a3[k] / ntiles, 100 * a3[k] / t3);
+    return 0;
+}
