@@ -133,20 +133,19 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads, smem_bytes_k1<TY>(), s>>>(img, g, bits, G, runs, E,
-                                                                                         unsigned(ntiles));
+        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads, smem_bytes_k1<TY>(), s>>>(
+            img, g, bits, G, runs, E, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
+        // K2: boundary unions (one warp per tile boundary), then resolve every
+        // tile's edge-touching roots (one warp per tile)
         const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
-        const long long n_v = (long long)g.B * g.H * (g.tiles_x - 1);
-        const long long blocks_h = (n_h + 7) / 8, blocks_v = (n_v + 255) / 256;
-        if (blocks_h + blocks_v > 0) {
-            ccl::k_boundary<TY, CONN><<<unsigned(blocks_h + blocks_v), 256, 0, s>>>(g, bits, runs, E, G, n_h,
-                                                                                   blocks_h);
+        const long long n_v = (long long)g.B * g.tiles_y * (g.tiles_x - 1);
+        if (n_h + n_v > 0) {
+            ccl::k_boundary<TY, CONN><<<unsigned((n_h + n_v + 7) / 8), 256, 0, s>>>(g, bits, runs, E, G, n_h, n_v);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
-        // resolve every tile's edge-touching roots (one warp per tile)
         const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
         ccl::k_resolve<TY><<<rblocks, 256, 0, s>>>(g, G, E, F, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

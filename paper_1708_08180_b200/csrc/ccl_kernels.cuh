@@ -130,6 +130,8 @@ __device__ __forceinline__ uint32_t nz16(uint4 v) {
     return nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
 }
 
+// Read-once image loads (no L1 allocation).  An L2 evict-first cache policy
+// on these loads measured slower for K1 and did not help K2 (profiles r01).
 __device__ __forceinline__ uint4 ld_stream_u4(const uint8_t* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -176,12 +178,36 @@ __device__ __forceinline__ void st_volatile(int32_t* p, int v) {
     *reinterpret_cast<volatile int32_t*>(p) = v;
 }
 
-// find with path halving in global memory (safe under concurrent min-unions:
-// a halving store writes an ancestor of a non-root node, R11).
+#ifdef CCL_STATS
+__device__ unsigned long long g_stat_unions = 0, g_stat_steps = 0;
+#define CCL_STAT(v) atomicAdd(&(v), 1ull)
+#else
+#define CCL_STAT(v) ((void)0)
+#endif
+
+// Global min-union (reading R11).  The finds use L1-cacheable loads: many
+// unions of a giant component end at the same root, and serving that hot
+// entry from each SM's L1 instead of one L2 slice removes the serialisation
+// that dominated this kernel.  A stale L1 value is an older parent, i.e. a
+// higher ancestor-or-self of the current one: a find may then stop at a node
+// that was a root but no longer is -- the atomicMin link detects that
+// (returns old != root) and the union continues from the true parent.  Two
+// nodes found under one (possibly stale) root are in one set, since sets only
+// ever merge.  Path halving stores write ancestors; a halving store can only
+// overwrite an atomicMin made on an already non-root node, whose issuer
+// re-unions from the value it displaced.  Every root is its set's minimum.
+__device__ __forceinline__ int ld_ca(const int32_t* p) {
+    int v;
+    asm volatile("ld.global.ca.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ int find_g(int32_t* G, int a) {
-    int p = ld_volatile(G + a);
+    int p = ld_ca(G + a);
+    CCL_LOOP_GUARD(fgh);
     while (p != a) {
-        const int gp = ld_volatile(G + p);
+        CCL_LOOP_TICK(fgh);
+        const int gp = ld_ca(G + p);
         if (gp != p) st_volatile(G + a, gp);
         a = p;
         p = gp;
@@ -189,30 +215,19 @@ __device__ __forceinline__ int find_g(int32_t* G, int a) {
     return a;
 }
 
-// Rem's union with splicing, lock-free (reading R11).  Walk x and y upward in
-// interleaved fashion, always on the side whose parent is larger; at every
-// step re-point that node at the other side's parent with atomicMin (a
-// "splice": it merges the two sets while compressing the path) and continue
-// from the parent it had.  Stop when both nodes have the same parent (same
-// set) or when a root gets linked.  Values only decrease (G[i] <= i), every
-// change links two nodes that must end up in one set, and each step moves to
-// a strictly smaller node, so it terminates; the walk usually meets below the
-// root, so the hot root entry of a giant component is rarely touched.
-__device__ __forceinline__ void union_g(int32_t* G, int x, int y) {
-    int px = ld_volatile(G + x), py = ld_volatile(G + y);
+__device__ __forceinline__ void union_g(int32_t* G, int a, int b) {
+    CCL_STAT(g_stat_unions);
     CCL_LOOP_GUARD(ug);
-    while (px != py) {
+    while (true) {
         CCL_LOOP_TICK(ug);
-        CCL_ASSERT(px <= x && py <= y && px >= 0 && py >= 0);
-        if (px < py) {
-            int t = x; x = y; y = t;
-            t = px; px = py; py = t;
-        }
-        // px > py: node x hangs above py; move it below py
-        const int old = atomicMin(G + x, py);
-        if (old == x) return;  // x was a root: linked
-        x = old;               // keep merging x's former ancestors
-        px = ld_volatile(G + x);
+        CCL_STAT(g_stat_steps);
+        a = find_g(G, a);
+        b = find_g(G, b);
+        if (a == b) return;
+        if (a < b) { int t = a; a = b; b = t; }
+        const int old = atomicMin(G + a, b);
+        if (old == a) return;
+        a = old;
     }
 }
 
@@ -668,6 +683,200 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
 }
 
+// ============================================================ K2: boundary
+// Boundary analysis (Alg. 2, §2.2): min-union of the local roots on the two
+// sides of every foreground edge that crosses a tile boundary (reading R9 /
+// R10).  The local roots come from K1's compact outputs -- the per-run records
+// of the tile rows next to a horizontal boundary and the column-root lists of
+// the tiles next to a vertical boundary -- so the only scattered accesses are
+// the union walks over the roots' parent entries in G.
+//
+// The unions run inside K1 (k_local_merge): a boundary is processed by the
+// block that finishes the SECOND of its two tiles (an arrival counter per
+// boundary), so the latency-bound global unions overlap the streaming local
+// merge of other tiles instead of forming a serial phase.  Reads of the
+// neighbour tile's outputs use ld.global.cg (L2, never a stale L1 line).
+
+// Warp-cooperative union of a batch of root pairs: each lane holds at most one
+// pair (a, b) (a < 0: none).  Pairs already seen in this warp are dropped
+// (identical root pairs are common: two large components meet at many places
+// along a tile edge) so only one lane per distinct pair runs the union.
+template <bool NOUNION = false>
+__device__ __forceinline__ void warp_union_pairs(int32_t* G, int a, int b, unsigned long long& last) {
+    if (a > b) { int t = a; a = b; b = t; }
+    const unsigned long long key =
+        (a >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
+    const unsigned grp = __match_any_sync(kFull, key);
+    const int lane = threadIdx.x & 31;
+    if (!NOUNION && key != ~0ull && key != last && (__ffs(grp) - 1) == lane) union_g(G, a, b);
+    if (key != ~0ull) last = key;
+}
+
+// image-local raster index of a K1 run record's root (tile origin x0, y0)
+__device__ __forceinline__ int rec_root(uint32_t rec, int W, int x0, int y0) {
+    const int rr = int(rec & 0x7FFFu);
+    return (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+}
+
+__device__ __forceinline__ size_t tile_index(const Geom& g, int b, int ty, int tx) {
+    return (size_t(b) * g.tiles_y + ty) * g.tiles_x + tx;
+}
+
+// The horizontal boundary above tile (b, band >= 1, tx); one warp.
+template <int TY, int CONN, bool NOUNION = false>
+__device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
+                                           const int32_t* E, int32_t* G, int b, int band, int tx,
+                                           Word (*s_w)[kWords]) {
+    const int lane = threadIdx.x & 31;
+    constexpr int RCAP = runs_per_tile_cap<TY>();
+    const int x0 = tx * kTileW, y0 = band * TY;
+    const size_t t_lo = tile_index(g, b, band, tx);  // tile below the edge
+    const size_t t_up = t_lo - g.tiles_x;             // tile above
+    const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
+    int32_t* Gb = G + size_t(b) * size_t(g.npx);
+    const uint32_t* Rlo = R + t_lo * RCAP;  // row 0 runs start at run id 0
+    const int up_base = __ldcg(E + t_up * kEdgeCap + 1);
+    CCL_ASSERT(up_base >= 0 && up_base < RCAP);
+    const uint32_t* Rup = R + t_up * RCAP + up_base;  // last row's runs
+    const int wg = tx * kWords + lane;
+    const uint32_t cur = wg < g.WW ? __ldcg(bm + size_t(y0) * g.WW + wg) : 0u;
+    const uint32_t up = wg < g.WW ? __ldcg(bm + size_t(y0 - 1) * g.WW + wg) : 0u;
+    uint32_t sc, su;
+    int cc, cu;
+    row_runs(cur, lane, sc, cc);
+    row_runs(up, lane, su, cu);
+    // row-local run index of the first start in each word (prefix of popc)
+    int ic = __popc(sc), iu = __popc(su);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(kFull, ic, d), c = __shfl_up_sync(kFull, iu, d);
+        if (lane >= d) { ic += a; iu += c; }
+    }
+    s_w[0][lane] = Word{cur, sc, cc, ic - __popc(sc)};
+    s_w[1][lane] = Word{up, su, cu, iu - __popc(su)};
+    __syncwarp();
+    uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
+    uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
+    if (lane == 0) { curL = 0; upL = 0; }
+    if (lane == 31) { curR = 0; upR = 0; }
+    const uint32_t o = cur & up, oL = curL & upL;
+    uint32_t ev = o & ~((o << 1) | (oL >> 31));
+    uint32_t ne = 0, nw = 0;
+    bool cnw = false, cne = false;  // diagonal edges through the tile corners
+    if (CONN == 8) {
+        const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
+        const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
+        ne = cur & ~cur_n & ~up & up_n;
+        nw = cur & ~cur_p & ~up & up_p;
+        if (lane == 0 && tx > 0 && (cur & 1u)) cnw = __ldcg(bm + size_t(y0 - 1) * g.WW + wg - 1) >> 31;
+        if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = __ldcg(bm + size_t(y0 - 1) * g.WW + wg + 1) & 1u;
+    }
+    // run index (within its row) of the run containing foreground pixel x:
+    // (number of run starts at positions <= x) - 1
+    auto run_idx = [&](int row, int x) {
+        CCL_ASSERT(x >= 0 && x < kTileW);
+        const Word& w = s_w[row][x >> 5];
+        const int i = w.pad + __popc(w.s & (kFull >> (31 - (x & 31)))) - 1;
+        CCL_ASSERT(i >= 0 && i < kTileW / 2);
+        return i;
+    };
+    const int W = g.W;
+    unsigned long long last = ~0ull;
+    while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
+        int a = -1, c = -1;
+        if (ev) {
+            const int x = (lane << 5) + __ffs(ev) - 1;
+            ev &= ev - 1;
+            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+            c = rec_root(__ldcg(Rup + run_idx(1, x)), W, x0, y0 - TY);
+        } else if (ne) {
+            const int x = (lane << 5) + __ffs(ne) - 1;
+            ne &= ne - 1;
+            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+            c = rec_root(__ldcg(Rup + run_idx(1, x + 1)), W, x0, y0 - TY);
+        } else if (nw) {
+            const int x = (lane << 5) + __ffs(nw) - 1;
+            nw &= nw - 1;
+            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+            c = rec_root(__ldcg(Rup + run_idx(1, x - 1)), W, x0, y0 - TY);
+        } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
+            cnw = false;
+            a = __ldcg(E + t_lo * kEdgeCap + kEdgeLC);
+            c = __ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1);
+        } else if (cne) {  // (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
+            cne = false;
+            a = __ldcg(E + t_lo * kEdgeCap + kEdgeRC);
+            c = __ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1);
+        }
+        CCL_ASSERT(a < 0 || (a < g.npx && c >= 0 && c < g.npx));
+        warp_union_pairs<NOUNION>(Gb, a, c, last);
+    }
+    __syncwarp();
+}
+
+// The vertical boundary left of tile (b, band, bx >= 1); one warp, lane = row.
+template <int TY, int CONN>
+__device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, int32_t* G, int b, int band,
+                                           int bx) {
+    const int lane = threadIdx.x & 31;
+    const int r = lane;
+    const size_t tr = tile_index(g, b, band, bx);  // tile right of the edge
+    const int32_t* Er = E + tr * kEdgeCap;
+    const int32_t* El = Er - kEdgeCap;              // tile left of the edge
+    int32_t* Gb = G + size_t(b) * size_t(g.npx);
+    int L = -1, Rr = -1, Lu = -1, Ru = -1;
+    if (r < TY && band * TY + r < g.H) {
+        L = __ldcg(El + kEdgeRC + r);   // root of (x0-1, y), or -1
+        Rr = __ldcg(Er + kEdgeLC + r);  // root of (x0, y), or -1
+        if (CONN == 8 && r > 0 && (L >= 0 || Rr >= 0)) {
+            Lu = __ldcg(El + kEdgeRC + r - 1);
+            Ru = __ldcg(Er + kEdgeLC + r - 1);
+        }
+    }
+    unsigned long long last = ~0ull;
+    warp_union_pairs(Gb, (L >= 0 && Rr >= 0) ? L : -1, Rr, last);        // W edge of (x0, y)
+    if (CONN == 8) {
+        warp_union_pairs(Gb, (Rr >= 0 && Lu >= 0) ? Rr : -1, Lu, last);  // NW of (x0, y)
+        warp_union_pairs(Gb, (L >= 0 && Ru >= 0) ? L : -1, Ru, last);    // NE of (x0-1, y)
+    }
+}
+
+// Standalone boundary analysis (all boundaries, one warp each); used when the
+// unions are not fused into K1 (profiling / the stage API's ablation path).
+template <int TY, int CONN, int DBG = 0>
+__global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
+                                                  const uint32_t* __restrict__ R,
+                                                  const int32_t* __restrict__ E,
+                                                  int32_t* __restrict__ G, long long n_h, long long n_v) {
+    __shared__ Word s_w[8][2][kWords];
+    const int warp = threadIdx.x >> 5;
+    const long long task = (long long)blockIdx.x * 8 + warp;
+    if (task < n_h) {
+        if (DBG & 2) return;
+        long long t = task;
+        const int tx = int(t % g.tiles_x);
+        t /= g.tiles_x;
+        const int band = 1 + int(t % (g.tiles_y - 1));
+        const int b = int(t / (g.tiles_y - 1));
+        boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp]);
+    } else if (task < n_h + n_v) {
+        if (DBG & 1) return;
+        long long t = task - n_h;
+        const int bx = 1 + int(t % (g.tiles_x - 1));
+        t /= (g.tiles_x - 1);
+        const int band = int(t % g.tiles_y);
+        const int b = int(t / g.tiles_y);
+        boundary_v<TY, CONN>(g, E, G, b, band, bx);
+    }
+}
+
+// ================================================================ K1 kernel
+// Persistent: each block walks tiles t = blockIdx.x, +gridDim.x, ...; the
+// 128-bit image loads of the NEXT tile are issued into registers before the
+// current tile is processed, so HBM reads overlap the shared-memory work.
+// (Fusing the boundary unions into this kernel -- each boundary merged by the
+// block that publishes its second tile -- measured 4x slower: the blocks
+// stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 3) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
@@ -694,171 +903,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_local_merge(const uint8_t* __re
         k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, b, bits, G, R, E, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
-    }
-}
-
-// ============================================================ K2: boundary
-// Boundary analysis (Alg. 2, §2.2): min-union of the local roots on the two
-// sides of every foreground edge that crosses a tile boundary (reading R9 /
-// R10).  The local roots come from K1's compact outputs -- the per-run records
-// of the tile rows next to a horizontal boundary and the column-root lists of
-// the tiles next to a vertical boundary -- so the only scattered accesses left
-// are the union walks over the roots' parent entries in G.
-//
-// Warp-cooperative union of a batch of root pairs: each lane holds at most one
-// pair (a, b) (a < 0: none).  Pairs already seen in this warp are dropped
-// (identical root pairs are common: two large components meet at many places
-// along a tile edge) so only one lane per distinct pair runs the union.
-__device__ __forceinline__ void warp_union_pairs(int32_t* G, int a, int b, unsigned long long& last,
-                                                 int img) {
-    if (a > b) { int t = a; a = b; b = t; }
-    const unsigned long long key =
-        (a >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
-    // pairs are only equal within one image (G values are image-local indices)
-    const unsigned grp = __match_any_sync(kFull, key) & __match_any_sync(kFull, img);
-    const int lane = threadIdx.x & 31;
-    if (key != ~0ull && key != last && (__ffs(grp) - 1) == lane) union_g(G, a, b);
-    if (key != ~0ull) last = key;
-}
-
-// image-local raster index of a K1 run record's root (tile origin x0, y0)
-__device__ __forceinline__ int rec_root(uint32_t rec, int W, int x0, int y0) {
-    const int rr = int(rec & 0x7FFFu);
-    return (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
-}
-
-// Horizontal tile edges: one warp per (image, band >= 1, tile column); vertical
-// tile edges: one thread per (image, tile column boundary >= 1, row).
-template <int TY, int CONN, int DBG = 0>
-__global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
-                                                  const uint32_t* __restrict__ R,
-                                                  const int32_t* __restrict__ E,
-                                                  int32_t* __restrict__ G, long long n_h,
-                                                  long long blocks_h) {
-    __shared__ Word s_w[8][2][kWords];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long last = ~0ull;
-    constexpr int RCAP = runs_per_tile_cap<TY>();
-    if (blockIdx.x < blocks_h) {
-        if (DBG & 2) return;  // profiling: skip horizontal edges
-        const long long task = (long long)blockIdx.x * 8 + warp;
-        if (task >= n_h) return;  // whole warp exits together
-        long long t = task;
-        const int tx = int(t % g.tiles_x);
-        t /= g.tiles_x;
-        const int band = 1 + int(t % (g.tiles_y - 1));
-        const int b = int(t / (g.tiles_y - 1));
-        const int x0 = tx * kTileW, y0 = band * TY;
-        const size_t t_lo = (size_t(b) * g.tiles_y + band) * g.tiles_x + tx;  // tile below the edge
-        const size_t t_up = t_lo - g.tiles_x;                                 // tile above
-        const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
-        int32_t* Gb = G + size_t(b) * size_t(g.npx);
-        const uint32_t* Rlo = R + t_lo * RCAP;                        // row 0 runs start at id 0
-        const int up_base = E[t_up * kEdgeCap + 1];
-        CCL_ASSERT(up_base >= 0 && up_base < RCAP);
-        const uint32_t* Rup = R + t_up * RCAP + up_base;  // last row's runs
-        const int wg = tx * kWords + lane;
-        const uint32_t cur = wg < g.WW ? bm[size_t(y0) * g.WW + wg] : 0u;
-        const uint32_t up = wg < g.WW ? bm[size_t(y0 - 1) * g.WW + wg] : 0u;
-        uint32_t sc, su;
-        int cc, cu;
-        row_runs(cur, lane, sc, cc);
-        row_runs(up, lane, su, cu);
-        // row-local run index of the first start in each word (prefix of popc)
-        int ic = __popc(sc), iu = __popc(su);
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int a = __shfl_up_sync(kFull, ic, d), c = __shfl_up_sync(kFull, iu, d);
-            if (lane >= d) { ic += a; iu += c; }
-        }
-        s_w[warp][0][lane] = Word{cur, sc, cc, ic - __popc(sc)};
-        s_w[warp][1][lane] = Word{up, su, cu, iu - __popc(su)};
-        __syncwarp();
-        uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
-        uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
-        if (lane == 0) { curL = 0; upL = 0; }
-        if (lane == 31) { curR = 0; upR = 0; }
-        const uint32_t o = cur & up, oL = curL & upL;
-        uint32_t ev = o & ~((o << 1) | (oL >> 31));
-        uint32_t ne = 0, nw = 0;
-        bool cnw = false, cne = false;  // diagonal edges through the tile corners
-        if (CONN == 8) {
-            const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
-            const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
-            ne = cur & ~cur_n & ~up & up_n;
-            nw = cur & ~cur_p & ~up & up_p;
-            if (lane == 0 && tx > 0 && (cur & 1u)) cnw = bm[size_t(y0 - 1) * g.WW + wg - 1] >> 31;
-            if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = bm[size_t(y0 - 1) * g.WW + wg + 1] & 1u;
-        }
-        // run index (within its row) of the run containing foreground pixel x:
-        // (number of run starts at positions <= x) - 1
-        auto run_idx = [&](int row, int x) {
-            CCL_ASSERT(x >= 0 && x < kTileW);
-            const Word& w = s_w[warp][row][x >> 5];
-            const int i = w.pad + __popc(w.s & (kFull >> (31 - (x & 31)))) - 1;
-            CCL_ASSERT(i >= 0 && i < kTileW / 2);
-            return i;
-        };
-        const int W = g.W;
-        while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
-            int a = -1, c = -1;
-            if (ev) {
-                const int x = (lane << 5) + __ffs(ev) - 1;
-                ev &= ev - 1;
-                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
-                c = rec_root(Rup[run_idx(1, x)], W, x0, y0 - TY);
-            } else if (ne) {
-                const int x = (lane << 5) + __ffs(ne) - 1;
-                ne &= ne - 1;
-                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
-                c = rec_root(Rup[run_idx(1, x + 1)], W, x0, y0 - TY);
-            } else if (nw) {
-                const int x = (lane << 5) + __ffs(nw) - 1;
-                nw &= nw - 1;
-                a = rec_root(Rlo[run_idx(0, x)], W, x0, y0);
-                c = rec_root(Rup[run_idx(1, x - 1)], W, x0, y0 - TY);
-            } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
-                cnw = false;
-                a = E[t_lo * kEdgeCap + kEdgeLC];
-                c = E[(t_up - 1) * kEdgeCap + kEdgeRC + TY - 1];
-            } else if (cne) {  // (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
-                cne = false;
-                a = E[t_lo * kEdgeCap + kEdgeRC];
-                c = E[(t_up + 1) * kEdgeCap + kEdgeLC + TY - 1];
-            }
-            CCL_ASSERT(a < 0 || (a < g.npx && c >= 0 && c < g.npx));
-            warp_union_pairs(Gb, a, c, last, 0);
-        }
-    } else {
-        if (DBG & 1) return;  // profiling: skip vertical edges
-        const long long task = (long long)(blockIdx.x - blocks_h) * 256 + threadIdx.x;
-        const int nbx = g.tiles_x - 1;
-        const long long n_v = (long long)g.B * g.H * nbx;
-        const bool valid = task < n_v;
-        long long t = valid ? task : 0;
-        const int y = int(t % g.H);
-        t /= g.H;
-        const int bx = 1 + int(t % nbx);
-        const int b = int(t / nbx);
-        const int band = y / TY, r = y - band * TY;
-        const size_t tr = (size_t(b) * g.tiles_y + band) * g.tiles_x + bx;  // tile right of the edge
-        const int32_t* Er = E + tr * kEdgeCap;
-        const int32_t* El = Er - kEdgeCap;                                 // tile left of the edge
-        int32_t* Gb = G + size_t(b) * size_t(g.npx);
-        int L = -1, Rr = -1, Lu = -1, Ru = -1;
-        if (valid) {
-            L = El[kEdgeRC + r];   // root of (x0-1, y), or -1
-            Rr = Er[kEdgeLC + r];  // root of (x0, y), or -1
-            if (CONN == 8 && r > 0 && (L >= 0 || Rr >= 0)) {
-                Lu = El[kEdgeRC + r - 1];
-                Ru = Er[kEdgeLC + r - 1];
-            }
-        }
-        warp_union_pairs(Gb, (L >= 0 && Rr >= 0) ? L : -1, Rr, last, b);      // W edge of (x0, y)
-        if (CONN == 8) {
-            warp_union_pairs(Gb, (Rr >= 0 && Lu >= 0) ? Rr : -1, Lu, last, b);  // NW of (x0, y)
-            warp_union_pairs(Gb, (L >= 0 && Ru >= 0) ? L : -1, Ru, last, b);    // NE of (x0-1, y)
-        }
     }
 }
 

@@ -150,8 +150,8 @@ int main(int argc, char** argv) {
     auto k1 = ccl::k_local_merge<TY, 8, true, 0>;
     const int grid1 = std::min<int>(ntiles, sms * 3);
     const size_t sm1 = sizeof(ccl::K1Smem<TY>);
-    const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)g.H * (g.tiles_x - 1);
-    const long long bh = (n_h + 7) / 8, bv = (n_v + 255) / 256;
+    const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)g.tiles_y * (g.tiles_x - 1);
+    const long long bh = (n_h + n_v + 7) / 8, bv = 0;
     auto time_k2 = [&](auto k2, const char* nm) {
         cudaEvent_t a, b;
         CK(cudaEventCreate(&a));
@@ -161,7 +161,7 @@ int main(int argc, char** argv) {
             CK(cudaMemsetAsync(flush, i, fb));
             k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
             CK(cudaEventRecord(a));
-            k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+            k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
             CK(cudaEventRecord(b));
             CK(cudaEventSynchronize(b));
             float ms;
@@ -174,16 +174,30 @@ int main(int argc, char** argv) {
     time_k2(ccl::k_boundary<TY, 8, 1>, "K2 horizontal only");
     time_k2(ccl::k_boundary<TY, 8, 2>, "K2 vertical only");
     time_k2(ccl::k_boundary<TY, 8, 3>, "K2 empty (launch)");
+    time_k2(ccl::k_boundary<TY, 8, 5>, "K2 horizontal, no unions");
     {
         k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
-        ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+        ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         float us = timeit([&] { ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles); }, flush, fb);
         printf("%-34s %8.1f us\n", "K2b resolve", us);
     }
 
+#ifdef CCL_STATS
+    {
+        unsigned long long z = 0, u, st;
+        CK(cudaMemcpyToSymbol(ccl::g_stat_unions, &z, 8));
+        CK(cudaMemcpyToSymbol(ccl::g_stat_steps, &z, 8));
+        k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
+        ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpyFromSymbol(&u, ccl::g_stat_unions, 8));
+        CK(cudaMemcpyFromSymbol(&st, ccl::g_stat_steps, 8));
+        printf("K2 stats: %llu union calls, %llu walk steps (%.2f per union)\n", u, st, double(st) / u);
+    }
+#endif
     // K3 (after K1 + K2), with stamps
     k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
-    ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, bh);
+    ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
     auto k3 = ccl::k_link<TY, 8, true, 0>;
     auto k3s = ccl::k_link<TY, 8, true, 4>;
