@@ -94,6 +94,16 @@ def workload(cfg: str, kind: str | None, rank: int, world: int, conn: int):
 
 
 # ------------------------------------------------------------------- helpers
+def load_traffic(workload: str, kernel: str):
+    """ncu-measured DRAM bytes per launch for this workload's kernel, if a
+    capture was committed under profiles/ (else None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
 def load_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -329,8 +339,11 @@ def run_ours(args, rank, world, local):
         bpp = {"k1_local_merge": K1_BYTES_PER_PX, "k3_link": K3_BYTES_PER_PX}.get(dom)
         if bpp is not None:
             ach = bpp * px_rank / (kern[dom] / 1e3) / 1e9
+            traffic = load_traffic(name, dom)
             line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
-                                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                                "unit": "GB/s", "frac": round(ach / peak, 4),
+                                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/)",
+                                "algorithmic_bytes_per_launch": int(bpp * px_rank),
                                 "bytes_per_px": bpp, "peak_source": peak_src,
                                 "share_of_step": round(kern[dom] / sum(kern.values()), 3)}
         else:
