@@ -140,6 +140,36 @@ ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H,
                                   int connectivity, int32_t* h_labels,
                                   void* d_scratch, size_t scratch_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Row-strip sharding of one image over k GPUs (north_star: "a single gigapixel
+ * image splits into row strips whose edge-row labels are exchanged with NCCL
+ * over NVLink, then merged by a cross-strip boundary-union and relabel pass").
+ * Rank r owns rows [row0, row0 + rows) of an H_total x W image (strips are
+ * contiguous and in rank order).  The result equals the unsharded labeling:
+ * labels are 1 + GLOBAL raster indices (H_total * W must be <= 2^31 - 1).
+ *
+ *   ccl_strip_local    (rank r) K1 + K2 on the strip; writes the 4*W-int send
+ *                      buffer: [0, W) labels of the strip's first row, [W, 2W)
+ *                      of its last row (0 = background), [2W, 4W) for each of
+ *                      those 2W slots the first slot with the same label.
+ *                      labels_out (rows * W int32, this rank's output) is used
+ *                      as scratch and must be passed unchanged to finalize.
+ *   caller             all-gather of the k send buffers into gathered
+ *                      (k * 4 * W int32, rank order) -- e.g. ncclAllGather.
+ *   ccl_strip_finalize (rank r) min-union over the k*2W slots (same-label slots
+ *                      of a strip; 4-/8-adjacent slots across every strip cut),
+ *                      patch the strip's edge-component labels, K3: labels_out.
+ * Workspace: >= ccl_strip_workspace_bytes(rows, W, k, connectivity), the same
+ * buffer for both calls.  Errors as above; CCL_ERR_DIMS also for rank/k/row0
+ * out of range. */
+size_t ccl_strip_workspace_bytes(int64_t rows, int64_t W, int k, int connectivity);
+ccl_status_t ccl_strip_local(const uint8_t* strip, int64_t rows, int64_t W, int64_t row0, int64_t H_total,
+                             int connectivity, int k, int32_t* send, int32_t* labels_out,
+                             void* workspace, size_t workspace_bytes, void* stream);
+ccl_status_t ccl_strip_finalize(const int32_t* gathered, int k, int rank, int64_t rows, int64_t W,
+                                int64_t row0, int64_t H_total, int connectivity, int32_t* labels_out,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

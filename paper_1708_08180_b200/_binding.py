@@ -36,6 +36,9 @@ SIGNATURES = {
     "ccl_boundary_work_items": (_i64, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "ccl_host_scratch_bytes": (_sz, [_i64, _i64, _i64, _int]),
     "ccl_label_host_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
+    "ccl_strip_workspace_bytes": (_sz, [_i64, _i64, _int, _int]),
+    "ccl_strip_local": (_int, [_vp, _i64, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _sz, _vp]),
+    "ccl_strip_finalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():
@@ -216,3 +219,74 @@ class HostSession:
     @property
     def d2h_bytes(self):
         return 4 * self.B * self.H * self.W
+
+
+# ------------------------------------------------------------- strip sharding
+class StripLabeler:
+    """Row-strip sharded labeling of one H_total x W image: this object owns
+    the per-rank buffers; ``local`` -> (caller all-gathers ``send``) ->
+    ``finalize``.  ``label`` does all three with torch.distributed."""
+
+    def __init__(self, rows: int, W: int, row0: int, H_total: int, k: int, rank: int,
+                 connectivity: int = 8, device=None):
+        torch = _torch()
+        self.rows, self.W, self.row0, self.H, self.k, self.rank, self.conn = rows, W, row0, H_total, k, rank, connectivity
+        n = int(_lib.ccl_strip_workspace_bytes(rows, W, k, connectivity))
+        if n == 0:
+            raise ValueError("invalid strip geometry")
+        dev = device or "cuda"
+        self.ws_bytes = n
+        self.ws = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.send = torch.empty(4 * W, dtype=torch.int32, device=dev)
+        self.gathered = torch.empty(k * 4 * W, dtype=torch.int32, device=dev)
+        self.out = torch.empty((rows, W), dtype=torch.int32, device=dev)
+
+    def local(self, strip, stream=None):
+        _check_image(strip)
+        _check(_lib.ccl_strip_local(ctypes.c_void_p(strip.data_ptr()), self.rows, self.W, self.row0, self.H,
+                                    self.conn, self.k, ctypes.c_void_p(self.send.data_ptr()),
+                                    ctypes.c_void_p(self.out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()),
+                                    self.ws_bytes, _stream_ptr(stream)), "ccl_strip_local")
+        return self.send
+
+    def finalize(self, gathered=None, stream=None):
+        g = self.gathered if gathered is None else gathered
+        _check(_lib.ccl_strip_finalize(ctypes.c_void_p(g.data_ptr()), self.k, self.rank, self.rows, self.W,
+                                       self.row0, self.H, self.conn, ctypes.c_void_p(self.out.data_ptr()),
+                                       ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream_ptr(stream)),
+               "ccl_strip_finalize")
+        return self.out
+
+    def label(self, strip, group=None):
+        """local -> NCCL all-gather of the 4W-int edge buffers -> finalize."""
+        import torch.distributed as dist
+        self.local(strip)
+        dist.all_gather_into_tensor(self.gathered, self.send, group=group)
+        return self.finalize()
+
+
+def strip_bounds(H: int, k: int, r: int):
+    """Rows [row0, row1) of strip r when H rows are split into k contiguous
+    strips as evenly as possible (the first H % k strips get one extra row)."""
+    base, extra = divmod(H, k)
+    row0 = r * base + min(r, extra)
+    return row0, row0 + base + (1 if r < extra else 0)
+
+
+def label_strips_emulated(image, k: int, connectivity: int = 8):
+    """Single-GPU emulation of k-way strip sharding (the all-gather becomes a
+    device copy): runs every rank's local and finalize stages on this GPU and
+    returns the assembled [H, W] labels (tests / smoke)."""
+    torch = _torch()
+    _check_image(image)
+    H, W = int(image.shape[0]), int(image.shape[1])
+    if not 1 <= k <= H:
+        raise ValueError("need 1 <= k <= H")
+    labelers = []
+    for r in range(k):
+        r0, r1 = strip_bounds(H, k, r)
+        lab = StripLabeler(r1 - r0, W, r0, H, k, r, connectivity, device=image.device)
+        lab.local(image[r0:r1])
+        labelers.append(lab)
+    gathered = torch.cat([lab.send for lab in labelers])
+    return torch.cat([lab.finalize(gathered) for lab in labelers])

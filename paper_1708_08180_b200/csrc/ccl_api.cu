@@ -2,6 +2,7 @@
 // workspace layout and the C ABI declared in include/ccl.h.
 #include "../../include/ccl.h"
 #include "ccl_kernels.cuh"
+#include "ccl_strip.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -46,6 +47,9 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.nwords = H * int64_t(p.g.WW);
     p.g.div_tx = ccl::FastDiv(unsigned(p.g.tiles_x));
     p.g.div_ty = ccl::FastDiv(unsigned(p.g.tiles_y));
+    p.g.label_off = 0;
+    p.g.force_top = 0;
+    p.g.force_bottom = 0;
     p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
     // per-run records: capacity of the worst case (alternating pixels) for the
@@ -90,7 +94,16 @@ cudaError_t setup_attrs() {
     return once;
 }
 
-enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7 };
+enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7, kStripEdges = 8, kStripFinalize = 16 };
+
+// Strip-mode arguments (row-strip sharding, ccl_strip_local / _finalize).
+struct StripCtx {
+    int32_t* send = nullptr;            // this rank's 4W send buffer
+    const int32_t* gathered = nullptr;  // k * 4W, rank order
+    int k = 1, rank = 0;
+    int32_t* P = nullptr;               // k * 2W slot parents
+    int32_t* minlab = nullptr;          // k * 2W
+};
 
 // Resident blocks per device for the persistent kernels K1 (which = 1) and
 // K3 (which = 3): SMs x blocks per SM at full occupancy, cached per
@@ -117,7 +130,7 @@ int persistent_blocks(int which) {
 
 template <int TY, int CONN, bool VEC>
 cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* out, void* ws,
-                       cudaStream_t s) {
+                       cudaStream_t s, const StripCtx* sc) {
     cudaError_t e = setup_attrs<TY, CONN, VEC>();
     if (e != cudaSuccess) return e;
     const ccl::Geom& g = p.g;
@@ -150,6 +163,26 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         ccl::k_resolve<TY><<<rblocks, 256, 0, s>>>(g, G, E, F, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
+    if (stages & kStripEdges) {
+        // edge-root marks (Gs = out as scratch), boundary-row labels, slot reps
+        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
+        ccl::k_strip_mark<TY><<<rblocks, 256, 0, s>>>(g, E, F, out, unsigned(ntiles));
+        ccl::k_strip_edges<TY><<<unsigned((2 * g.tiles_x + 7) / 8), 256, 0, s>>>(g, bits, runs, E, F, sc->send, out);
+        const unsigned sb = unsigned(std::min(1184, (2 * g.W + 255) / 256));
+        ccl::k_strip_min<<<sb, 256, 0, s>>>(sc->send, out, g.W, g.label_off);
+        ccl::k_strip_rep<<<sb, 256, 0, s>>>(sc->send, out, g.W, g.label_off);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (stages & kStripFinalize) {
+        const int n = sc->k * 2 * g.W;
+        const unsigned sb = unsigned(std::min(1184, (n + 255) / 256));
+        ccl::k_slots_init<<<sb, 256, 0, s>>>(sc->P, sc->minlab, n);
+        ccl::k_slots_union<CONN><<<sb, 256, 0, s>>>(sc->gathered, sc->P, sc->k, g.W);
+        ccl::k_slots_minlab<<<sb, 256, 0, s>>>(sc->gathered, sc->P, sc->minlab, sc->k, g.W);
+        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
+        ccl::k_strip_patch<TY><<<rblocks, 256, 0, s>>>(g, E, F, out, sc->P, sc->minlab, sc->rank, unsigned(ntiles));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if (stages & kK3) {
         ccl::k_link<TY, CONN, VEC><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -159,12 +192,12 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
 
 template <int TY>
 cudaError_t dispatch_conn(const Plan& p, int conn, bool vec, int stages, const uint8_t* img,
-                          int32_t* out, void* ws, cudaStream_t s) {
+                          int32_t* out, void* ws, cudaStream_t s, const StripCtx* sc) {
     if (conn == 4)
-        return vec ? run_stages<TY, 4, true>(p, stages, img, out, ws, s)
-                   : run_stages<TY, 4, false>(p, stages, img, out, ws, s);
-    return vec ? run_stages<TY, 8, true>(p, stages, img, out, ws, s)
-               : run_stages<TY, 8, false>(p, stages, img, out, ws, s);
+        return vec ? run_stages<TY, 4, true>(p, stages, img, out, ws, s, sc)
+                   : run_stages<TY, 4, false>(p, stages, img, out, ws, s, sc);
+    return vec ? run_stages<TY, 8, true>(p, stages, img, out, ws, s, sc)
+               : run_stages<TY, 8, false>(p, stages, img, out, ws, s, sc);
 }
 
 // The 128-bit paths need 16-byte aligned rows: W % 16 == 0 for the uint8 image
@@ -177,13 +210,13 @@ bool vector_ok(const Plan& p, const void* img, const void* out) {
 }
 
 ccl_status_t run(const Plan& p, int conn, int stages, const uint8_t* img, int32_t* out, void* ws,
-                 cudaStream_t s) {
+                 cudaStream_t s, const StripCtx* sc = nullptr) {
     const bool vec = vector_ok(p, img, out);
     cudaError_t e;
     switch (p.ty) {
-        case 8: e = dispatch_conn<8>(p, conn, vec, stages, img, out, ws, s); break;
-        case 16: e = dispatch_conn<16>(p, conn, vec, stages, img, out, ws, s); break;
-        case 32: e = dispatch_conn<32>(p, conn, vec, stages, img, out, ws, s); break;
+        case 8: e = dispatch_conn<8>(p, conn, vec, stages, img, out, ws, s, sc); break;
+        case 16: e = dispatch_conn<16>(p, conn, vec, stages, img, out, ws, s, sc); break;
+        case 32: e = dispatch_conn<32>(p, conn, vec, stages, img, out, ws, s, sc); break;
         default: return CCL_ERR_CONFIG;
     }
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
@@ -353,6 +386,67 @@ ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H,
     e = cudaMemcpyAsync(h_labels, d_out, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e);
     return CCL_OK;
+}
+
+// ------------------------------------------------------- strip sharding
+static size_t align_up_c(size_t v) { return (v + 255) / 256 * 256; }
+
+size_t ccl_strip_workspace_bytes(int64_t rows, int64_t W, int k, int connectivity) {
+    Plan p;
+    if (k < 1 || make_plan(1, rows, W, connectivity, 0, p) != CCL_OK) return 0;
+    return p.total() + 2 * align_up_c(size_t(k) * 2 * size_t(W) * sizeof(int32_t));
+}
+
+static ccl_status_t strip_plan(int64_t rows, int64_t W, int64_t row0, int64_t H_total, int conn, int k,
+                               int rank, Plan& p) {
+    if (k < 1 || rank < 0 || rank >= k) return CCL_ERR_DIMS;
+    if (rows < 1 || W < 1 || row0 < 0 || H_total < 1 || row0 + rows > H_total) return CCL_ERR_DIMS;
+    if (H_total > INT32_MAX / W) return CCL_ERR_TOO_LARGE;  // labels are global raster indices
+    if (int64_t(k) * 4 * W > INT32_MAX) return CCL_ERR_TOO_LARGE;
+    ccl_status_t st = make_plan(1, rows, W, conn, 0, p);
+    if (st != CCL_OK) return st;
+    p.g.label_off = int(row0 * W);
+    p.g.force_top = row0 > 0;
+    p.g.force_bottom = row0 + rows < H_total;
+    return CCL_OK;
+}
+
+ccl_status_t ccl_strip_local(const uint8_t* strip, int64_t rows, int64_t W, int64_t row0, int64_t H_total,
+                             int connectivity, int k, int32_t* send, int32_t* labels_out, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+    Plan p;
+    ccl_status_t st = strip_plan(rows, W, row0, H_total, connectivity, k, 0, p);
+    if (st != CCL_OK) return st;
+    if (!send) return CCL_ERR_NULL;
+    st = validate_buffers(p, strip, labels_out, workspace, workspace_bytes, kAll);
+    if (st != CCL_OK) return st;
+    if (workspace_bytes < ccl_strip_workspace_bytes(rows, W, k, connectivity)) return CCL_ERR_WORKSPACE;
+    StripCtx sc;
+    sc.send = send;
+    sc.k = k;
+    return run(p, connectivity, kK1 | kK2 | kStripEdges, strip, labels_out, workspace,
+               static_cast<cudaStream_t>(stream), &sc);
+}
+
+ccl_status_t ccl_strip_finalize(const int32_t* gathered, int k, int rank, int64_t rows, int64_t W, int64_t row0,
+                                int64_t H_total, int connectivity, int32_t* labels_out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    Plan p;
+    ccl_status_t st = strip_plan(rows, W, row0, H_total, connectivity, k, rank, p);
+    if (st != CCL_OK) return st;
+    if (!gathered) return CCL_ERR_NULL;
+    st = validate_buffers(p, nullptr, labels_out, workspace, workspace_bytes, kK3);
+    if (st != CCL_OK) return st;
+    if (workspace_bytes < ccl_strip_workspace_bytes(rows, W, k, connectivity)) return CCL_ERR_WORKSPACE;
+    StripCtx sc;
+    sc.gathered = gathered;
+    sc.k = k;
+    sc.rank = rank;
+    char* slots = static_cast<char*>(workspace) + p.total();
+    sc.P = reinterpret_cast<int32_t*>(slots);
+    sc.minlab = reinterpret_cast<int32_t*>(slots + align_up_c(size_t(k) * 2 * size_t(W) * sizeof(int32_t)));
+    return run(p, connectivity, kStripFinalize | kK3, nullptr, labels_out, workspace,
+               static_cast<cudaStream_t>(stream), &sc);
 }
 
 }  // extern "C"

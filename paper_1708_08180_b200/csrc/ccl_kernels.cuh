@@ -73,6 +73,10 @@ struct Geom {
     long long npx;     // H*W  (per image)
     long long nwords;  // H*WW (per image)
     FastDiv div_tx, div_ty;  // by tiles_x, tiles_y
+    // strip mode (row-strip sharding of one image over several GPUs):
+    int label_off;     // added to every label (row0 * W_total: labels are global)
+    int force_top;     // the image's first row borders another strip
+    int force_bottom;  // the image's last row borders another strip
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -590,11 +594,15 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // conversion): flag the roots of top / bottom row runs and of left / right
     // column pixels; record the column pixels' roots for the boundary analysis.
     const int W = g.W, x0 = id.x0, y0 = id.y0;
-    const bool top = y0 > 0, bottom = y0 + TY < g.H, left = x0 > 0, right = x0 + kTileW < W;
+    // rows that border another tile (or, in strip mode, another strip)
+    const int last_row = min(TY, g.H - y0) - 1;
+    const bool top = y0 > 0 || g.force_top;
+    const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
+    const bool left = x0 > 0, right = x0 + kTileW < W;
     for (int k = tid; k < total; k += kThreads) {
         const int rsk = sm.rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
-        const bool hrow = (r == 0 && top) || (r == TY - 1 && bottom);
+        const bool hrow = (r == 0 && top) || (r == last_row && bottom);
         const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
         if (hrow || lc || rc) {
             const int root = sm.P[k];
@@ -648,7 +656,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // loads hit fully valid L2 sectors instead of filling from DRAM.
     int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
     int32_t* Eh = E + size_t(t) * kEdgeCap;
-    if (tid == 0) Eh[1] = sm.rbase[TY - 1];
+    if (tid == 0) Eh[1] = sm.rbase[min(TY, g.H - y0) - 1];  // first run of the last valid row
     if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
     else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
@@ -920,7 +928,7 @@ __global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restri
         const int32_t* Et = E + size_t(t) * kEdgeCap;
         const int n = Et[0];
         const int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
-        for (int i = lane; i < n; i += 32) F[size_t(t) * kEdgeCap + i] = find_g_ro(Gb, Et[kEdgeList + i]) + 1;
+        for (int i = lane; i < n; i += 32) F[size_t(t) * kEdgeCap + i] = find_g_ro(Gb, Et[kEdgeList + i]) + 1 + g.label_off;
     }
 }
 
@@ -985,7 +993,7 @@ __device__ __forceinline__ void k3_tile(TileSmem<TY>& sm, const Geom& g, unsigne
             const uint32_t v = k < kRunCache ? sm.rc[k] : __ldg(Rt + k);
             const int e = int(v >> 16);  // 1 + edge-list index, or 0
             const int rr = int(v & 0x7FFFu);
-            int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1;
+            int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
             if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
             sm.P[l >> 1] = lab | kTag;
         });

@@ -22,7 +22,7 @@ import numpy as np
 __all__ = [
     "GAMMA", "mix64", "noise", "texture", "blobs", "upscaled", "spiral",
     "serpentine", "checkerboard", "stripes", "diagonal", "uniform",
-    "frames", "percolation_density",
+    "frames", "percolation_density", "upscaled_rows",
 ]
 
 GAMMA = np.uint64(0x9E3779B97F4A7C15)
@@ -136,6 +136,17 @@ def upscaled(H: int, W: int, seed: int, factor: int = 16, density: float = 0.5) 
         raise ValueError("H and W must be multiples of factor")
     base = texture(H // factor, W // factor, seed, density, octaves=((32, 4), (8, 2), (2, 1)))
     return np.repeat(np.repeat(base, factor, axis=0), factor, axis=1)
+
+
+def upscaled_rows(H: int, W: int, seed: int, r0: int, r1: int, factor: int = 16,
+                  density: float = 0.5) -> np.ndarray:
+    """Rows [r0, r1) of ``upscaled(H, W, seed, factor, density)`` without
+    materialising the whole image (row-strip sharded gigapixel inputs, C5)."""
+    if H % factor or W % factor:
+        raise ValueError("H and W must be multiples of factor")
+    base = texture(H // factor, W // factor, seed, density, octaves=((32, 4), (8, 2), (2, 1)))
+    rows = base[np.arange(r0, r1) // factor]
+    return np.repeat(rows, factor, axis=1)
 
 
 def spiral(H: int, W: int) -> np.ndarray:

@@ -151,3 +151,32 @@ def test_import_fails_loudly_without_library(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_1708_08180_b200"], cwd=tmp_path,
                        capture_output=True, text=True)
     assert r.returncode != 0 and "missing" in r.stderr
+
+
+def test_strip_validation(ccl):
+    L = ccl.raw()
+    need = L.ccl_strip_workspace_bytes(64, 1024, 4, 8)
+    assert need > ccl.workspace_bytes(1, 64, 1024, 8)
+    assert L.ccl_strip_workspace_bytes(64, 1024, 0, 8) == 0
+    # rank / k / row0 out of range
+    assert L.ccl_strip_finalize(FAKE_A, 4, 4, 64, 1024, 0, 256, 8, FAKE_B, FAKE_WS, need, None) == 2
+    assert L.ccl_strip_local(FAKE_A, 64, 1024, 200, 256, 8, 4, FAKE_B, ctypes.c_void_p(0x40000000),
+                             FAKE_WS, need, None) == 2
+    # global labels must fit int32
+    assert L.ccl_strip_local(FAKE_A, 64, 65536, 0, 40000, 8, 4, FAKE_B, ctypes.c_void_p(0x40000000),
+                             FAKE_WS, need, None) == 3
+    # workspace too small
+    assert L.ccl_strip_local(FAKE_A, 64, 1024, 0, 256, 8, 4, FAKE_B, ctypes.c_void_p(0x40000000),
+                             FAKE_WS, need - 1, None) == 6
+
+
+def test_strip_bounds_partition(ccl):
+    for H in (1, 7, 8, 100, 1080, 32768):
+        for k in (1, 2, 3, 4, 8):
+            if k > H:
+                continue
+            spans = [ccl.strip_bounds(H, k, r) for r in range(k)]
+            assert spans[0][0] == 0 and spans[-1][1] == H
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1

@@ -254,3 +254,36 @@ def test_degenerate(ccl):
                 assert_same(gpu_label(ccl, img, conn), oracle.label_bfs(img, conn), f"{H}x{W}={v}")
     empty = torch.empty((0, 5, 5), dtype=torch.uint8, device="cuda")
     assert ccl.label(empty, 8).shape == (0, 5, 5)
+
+
+# ------------------------------------------ row-strip sharding
+@pytest.mark.parametrize("conn", CONNS)
+def test_strips_emulated(ccl, conn):
+    """k-way strip sharding emulated on one GPU (the all-gather is a device
+    copy) must equal the unsharded canonical labeling (T6 of SURVEY.md §4)."""
+    import torch
+    cases = [
+        ("texture", synth.texture(600, 2100, seed=4, density=0.5), (1, 2, 3, 4, 8)),
+        ("noise", synth.noise(257, 1031, 0.55, seed=5), (2, 5, 7)),
+        ("spiral", synth.spiral(120, 300), (2, 3, 8)),
+        ("serpentine", synth.serpentine(97, 2049), (2, 4, 8)),
+        ("vstripes", synth.stripes(64, 1030, 2, True), (8,)),
+        ("checker", synth.checkerboard(33, 1025), (4,)),
+        ("uniform", synth.uniform(40, 700), (5,)),
+        ("rows1", synth.noise(8, 3000, 0.6, seed=6), (8,)),
+    ]
+    for name, img, ks in cases:
+        want = oracle.label_bfs(img, conn)
+        t = torch.from_numpy(img).cuda()
+        for k in ks:
+            got = ccl.label_strips_emulated(t, k, conn).cpu().numpy()
+            assert_same(got, want, f"strips {name} k={k}")
+
+
+def test_strips_c5_shape_sampled(ccl):
+    """C5-like geometry at reduced height (full width 32768): 8 strips."""
+    import torch
+    img = synth.texture(512, 32768, seed=5001, density=0.5)
+    t = torch.from_numpy(img).cuda()
+    got = ccl.label_strips_emulated(t, 8, 8).cpu().numpy()
+    assert_same(got, oracle.label_bfs(img, 8), "C5-like strips")

@@ -116,6 +116,7 @@ int main(int argc, char** argv) {
     const unsigned ntiles = g.tiles_x * g.tiles_y;
     g.div_tx = ccl::FastDiv(g.tiles_x);
     g.div_ty = ccl::FastDiv(g.tiles_y);
+    g.label_off = g.force_top = g.force_bottom = 0;
     for (int per_sm : {2, 3}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
