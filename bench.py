@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--kind", default=None, help="C3 generator: texture|blobs|upscaled|noise|perc")
     ap.add_argument("--conn", type=int, default=8, choices=[4, 8])
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--tile-rows", type=int, default=0, help="K1 tile height (8/16/32; 0 = library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
@@ -274,7 +275,7 @@ def run_ours(args, rank, world, local):
     launches_per_step = 3 + (1 if nh + nv > 0 else 0)  # K1, [K2 boundary], K2 resolve, K3
 
     def step():
-        ccl.label(img, conn, out=out, workspace=ws)
+        ccl.label(img, conn, out=out, workspace=ws, tile_rows=args.tile_rows)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -314,7 +315,7 @@ def run_ours(args, rank, world, local):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record(stream)
             for j, f in enumerate(ks):
-                f(img, conn, out, ws)
+                f(img, conn, out, ws, args.tile_rows)
                 e[j + 1].record(stream)
             torch.cuda.synchronize()
             for j in range(3):
@@ -332,7 +333,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": name, "connectivity": conn, "B": B, "H": H, "W": W, "gen": desc["gen"],
                    "px_per_rank": px_rank, "parallelism": f"dp{world} (independent images, no collective)",
                    "l2": f"flushed: {args.flush_mb} MiB memset before every timed step (outside events)",
-                   "tile": "1024x16"},
+                   "tile": f"1024x{args.tile_rows or 16}"},
         "per_gpu_mpx_s": round(px_rank / (ms / 1e3) / 1e6, 2),
         "wall_ms_per_step_incl_flush": round(1e3 * wall / K, 4),
         "step_ms": {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),

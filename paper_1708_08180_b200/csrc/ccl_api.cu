@@ -4,8 +4,11 @@
 #include "ccl_kernels.cuh"
 #include "ccl_strip.cuh"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 
 namespace {
 
@@ -75,7 +78,7 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 template <int TY>
-size_t smem_bytes() { return sizeof(ccl::TileSmem<TY>); }
+size_t smem_bytes() { return sizeof(ccl::LinkSmem<TY>); }
 template <int TY>
 size_t smem_bytes_k1() { return sizeof(ccl::K1Smem<TY>); }
 
@@ -87,11 +90,40 @@ cudaError_t setup_attrs() {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem_bytes_k1<TY>()));
         if (e != cudaSuccess) return e;
-        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem_bytes<TY>()));
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem_bytes<TY>()));
     }();
     return once;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// TMA descriptor of the int32 label tensor viewed as [B*H][W/32][32] with a
+// [1][32][32] box (one 1024-px tile row) and 128-byte swizzle (W % 32 == 0).
+bool encode_label_map(CUtensorMap* map, int32_t* out, const ccl::Geom& g) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {32, cuuint64_t(g.W / 32), cuuint64_t(g.B) * cuuint64_t(g.H)};
+    const cuuint64_t strides[2] = {128, cuuint64_t(g.W) * 4};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7, kStripEdges = 8, kStripFinalize = 16 };
@@ -122,7 +154,7 @@ int persistent_blocks(int which) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads,
                                                       smem_bytes_k1<TY>());
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC>, ccl::kThreads,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC, true>, ccl::kThreads,
                                                       smem_bytes<TY>());
     cached[w][dev] = std::max(1, sms) * std::max(1, b);
     return cached[w][dev];
@@ -184,7 +216,16 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK3) {
-        ccl::k_link<TY, CONN, VEC><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out, unsigned(ntiles));
+        // labels leave through TMA bulk-tensor stores when rows are 32-px
+        // multiples (all bench configs); else 128-bit st.global.cs
+        CUtensorMap map;
+        std::memset(&map, 0, sizeof(map));
+        if (VEC && g.W % 32 == 0 && encode_label_map(&map, out, g))
+            ccl::k_link<TY, CONN, VEC, true><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out,
+                                                                              unsigned(ntiles), map);
+        else
+            ccl::k_link<TY, CONN, VEC, false><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out,
+                                                                               unsigned(ntiles), map);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -31,6 +31,7 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded on the host in ccl_api.cu)
 #include <cuda_runtime.h>
 
 #ifdef CCL_CHECK
@@ -110,18 +111,6 @@ constexpr int kEdgeRC = 34;
 constexpr int kEdgeList = 66;
 constexpr int kEdgeCap = 1152;
 constexpr int kEdgeCache = 32;  // resolved labels K3 prefetches per tile
-
-// Shared-memory layout of one K3 tile (dynamic shared memory).
-template <int TY>
-struct TileSmem {
-    Word wd[TY][kWords];        // .pad = row-local index of the word's first run
-    int32_t P[TY * kTileW / 2]; // index (l>>1) of a run start l: its final label (tagged)
-    int32_t rcnt[TY];           // runs per tile row
-    uint32_t rc[kRunCache];     // K3: first run records of the tile (prefetched)
-    int32_t fc[kEdgeCache];     // K3: first resolved edge labels (prefetched)
-};
-
-
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t nz4(uint32_t w) {
@@ -265,67 +254,6 @@ __device__ __forceinline__ TileId decode_tile(const Geom& g, unsigned t) {
     id.x0 = id.tx * kTileW;
     id.y0 = id.ty * TY;
     return id;
-}
-
-// ------------------------------------------- K1 / K3 shared local labeling
-// Phase L1: masks -> smem, run starts, carries, parent init.  `m` is this
-// lane's mask word of tile row r.
-template <int TY, bool INIT_P>
-__device__ __forceinline__ void tile_row_init(TileSmem<TY>& sm, int r, int lane, uint32_t m) {
-    uint32_t s;
-    int c;
-    row_runs(m, lane, s, c);
-    // row-local run index of this word's first run start (exclusive prefix)
-    const int n = __popc(s);
-    int incl = n;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
-    }
-    Word wd;
-    wd.m = m;
-    wd.s = s;
-    wd.c = c;
-    wd.pad = incl - n;
-    sm.wd[r][lane] = wd;
-    if (lane == 31) sm.rcnt[r] = incl;
-    if (INIT_P) {
-        const int base = r * kTileW + (lane << 5);
-        uint32_t t = s;
-        while (t) {
-            const int bit = __ffs(t) - 1;
-            t &= t - 1;
-            const int l = base + bit;
-            sm.P[l >> 1] = l;
-        }
-    }
-}
-
-// Tile-local index of the first run of tile row r (prefix of rcnt; after a
-// barrier that follows tile_row_init of all rows).
-template <int TY>
-__device__ __forceinline__ int row_run_base(const TileSmem<TY>& sm, int r, int lane) {
-    int v = lane < TY ? sm.rcnt[lane] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(kFull, v, d);
-        if (lane >= d) v += t;
-    }
-    const int incl = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0);
-    return r > 0 ? incl : 0;
-}
-
-// Calls f(l) for every run start l of tile row r held by this lane.
-template <int TY, typename F>
-__device__ __forceinline__ void for_each_run_start(const TileSmem<TY>& sm, int r, int lane, F f) {
-    uint32_t t = sm.wd[r][lane].s;
-    const int base = r * kTileW + (lane << 5);
-    while (t) {
-        const int bit = __ffs(t) - 1;
-        t &= t - 1;
-        f(base + bit);
-    }
 }
 
 // =========================================================== K1: local merge
@@ -549,6 +477,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
             }
         }
     }
+#pragma unroll 1
     for (int k = tid; k < total; k += kThreads) sm.P[k] = k;
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
@@ -563,6 +492,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // right of k's start, so it cannot reach k-1.  Each run therefore does at
     // most two unions, found in O(1) from the masks: no fan-in serialisation.
     constexpr int D = CONN == 8 ? 1 : 0;
+#pragma unroll 1
     for (int k = tid; k < total; k += kThreads) {
         const int rsk = sm.rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
@@ -582,30 +512,26 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
-    for (int k = tid; k < total; k += kThreads) sm.P[k] = find_r_ro(sm.P, k);
-    __syncthreads();
+    // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
+    // index conversion): every run points at its root; the roots of top /
+    // bottom row runs and of left / right column pixels are flagged and the
+    // column pixels' roots recorded for the boundary analysis.
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
-    if (DBG & 2) {
-        __syncthreads();
-        return;
-    }
-
-    // Alg. 1 l.34-39 for tile-edge items only (reading R7 for the index
-    // conversion): flag the roots of top / bottom row runs and of left / right
-    // column pixels; record the column pixels' roots for the boundary analysis.
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     // rows that border another tile (or, in strip mode, another strip)
     const int last_row = min(TY, g.H - y0) - 1;
     const bool top = y0 > 0 || g.force_top;
     const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
     const bool left = x0 > 0, right = x0 + kTileW < W;
+#pragma unroll 1
     for (int k = tid; k < total; k += kThreads) {
+        const int root = find_r_ro(sm.P, k);
+        sm.P[k] = root;  // an ancestor: concurrent finds stay valid
         const int rsk = sm.rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
         const bool hrow = (r == 0 && top) || (r == last_row && bottom);
         const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
         if (hrow || lc || rc) {
-            const int root = sm.P[k];
             atomicOr(&sm.flag[root >> 5], 1u << (root & 31));
             if (lc || rc) {
                 const int rr = sm.rs[root];
@@ -614,6 +540,11 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
                 if (rc) sm.rc[r] = gr;
             }
         }
+    }
+    if (DBG & 2) {
+        __syncthreads();
+        __syncthreads();
+        return;
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
@@ -661,6 +592,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
     int32_t* Et = Eh + kEdgeList;
+#pragma unroll 1
     for (int k = tid; k < total; k += kThreads) {
         const int root = sm.P[k];
         const int rr = sm.rs[root];  // row*1024 + x of the root run's start
@@ -933,12 +865,35 @@ __global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restri
 }
 
 // ================================================================ K3: link
-// Final link (§2.3): the tile's runs are re-derived from the bit mask (run
-// starts only, no union-find) and take their local root from K1's per-run
-// records; roots whose component touches a tile edge are resolved through G
-// (find); then every pixel gets 1 + its global root, or 0.
-// Persistent like K1: the next tile's mask words and first kRunCache run
-// records are prefetched into registers while the current tile is written.
+// Final link (§2.3).  Per tile:
+//  1. row runs re-derived from the bit mask (start masks + run numbering only,
+//     no union-find);
+//  2. one thread per run: final label = 1 + global root (K1's per-run record),
+//     or the boundary analysis' resolved label when the component touches a
+//     tile edge -> label table lab[run id];
+//  3. per tile row, every lane expands its own 32-px word into labels (the
+//     label changes only at run starts, so a 4-px group costs one test in the
+//     common case) into a per-warp shared-memory row buffer (XOR-swizzled:
+//     conflict-free 128-bit stores and loads), then the warp streams the row
+//     out with coalesced 128-bit evict-first stores (512 contiguous bytes per
+//     warp instruction).
+// Persistent like K1: the next tile's mask words, first run records and first
+// resolved labels are prefetched into registers while the current tile is
+// processed.
+template <int TY>
+struct __align__(1024) LinkSmem {
+    // per-warp row of labels in the TMA SWIZZLE_128B layout: the 1024-px row is
+    // a 32 x 128 B box (one 128-B row per 32-px word); 16-B unit q of word w
+    // sits at w*128 + ((q ^ (w & 7)) * 16) -- also conflict-free for the lanes
+    int4 rowbuf[kWarps][kTileW / 4];
+    Word wd[TY][kWords];             // .m mask, .s run starts, .pad runs before the word
+    int32_t lab[TY * kTileW / 2];    // final label of tile run k
+    uint4 rc[kRunCache / 4];         // first run records of the tile (prefetched)
+    int32_t fc[kEdgeCache];          // first resolved edge labels (prefetched)
+    int32_t rcnt[TY];
+    int32_t rbase[TY + 1];
+};
+
 template <int TY>
 struct LinkRegs {
     uint32_t m[TY / kWarps];
@@ -964,90 +919,146 @@ __device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t
     if (warp == 1) pf.fin = __ldg(F + size_t(t) * kEdgeCap + lane);
 }
 
-template <int TY, int CONN, bool VEC, int DBG = 0>
-__device__ __forceinline__ void k3_tile(TileSmem<TY>& sm, const Geom& g, unsigned t, const LinkRegs<TY>& cur,
-                                        const uint32_t* R, const int32_t* F, int32_t* out, int warp,
-                                        int lane) {
+// TMA bulk-tensor store of one 1024-px label row from shared memory: the
+// labels tensor is viewed as [rows][W/32][32] int32, the box is [1][32][32]
+// (out-of-range chunks of the last tile column are clipped by the hardware).
+__device__ __forceinline__ void tma_store_row(const CUtensorMap* tmap, const void* smem, int chunk0, int row) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(0), "r"(chunk0), "r"(row), "r"(sa)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 16-byte slot of 4-px group q (0..255) of a row in the swizzled row buffer:
+// group q = 8*w + g (word w, group g within the word) lives at 8*w + (g ^ (w & 7)).
+__device__ __forceinline__ int swz(int w, int g) { return (w << 3) + (g ^ (w & 7)); }
+
+template <int TY, int CONN, bool VEC, bool TMA, int DBG = 0>
+__device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, unsigned t, const LinkRegs<TY>& cur,
+                                        const uint32_t* R, const int32_t* F, int32_t* out,
+                                        const CUtensorMap* tmap, int warp, int lane) {
     const TileId id = decode_tile<TY>(g, t);
     int32_t* ob = out + size_t(id.b) * size_t(g.npx);
     const uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
     const int32_t* Ft = F + size_t(t) * kEdgeCap;
+    const int tid = threadIdx.x;
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 0);
 
-    if (warp == 0 || warp == 2) reinterpret_cast<uint4*>(sm.rc)[lane + (warp == 2 ? 32 : 0)] = cur.runs;
+    if (warp == 0 || warp == 2) sm.rc[lane + (warp == 2 ? 32 : 0)] = cur.runs;
     if (warp == 1) sm.fc[lane] = cur.fin;
+    // 1. run starts and run numbering of every row
 #pragma unroll
-    for (int i = 0; i < TY / kWarps; ++i) tile_row_init<TY, false>(sm, warp + i * kWarps, lane, cur.m[i]);
+    for (int i = 0; i < TY / kWarps; ++i) {
+        const int r = warp + i * kWarps;
+        const uint32_t m = cur.m[i];
+        uint32_t pm = __shfl_up_sync(kFull, m, 1);
+        if (lane == 0) pm = 0;
+        const uint32_t s = m & ~((m << 1) | (pm >> 31));
+        const int n = __popc(s);
+        int incl = n;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += u;
+        }
+        sm.wd[r][lane] = Word{m, s, 0, incl - n};
+        if (lane == 31) sm.rcnt[r] = incl;
+    }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 1);
-
-    // every run start gets its final label: 1 + the global root, which is the
-    // local root (from K1's record) unless the component touches a tile edge,
-    // then it is the boundary analysis' resolved label
+    // 2. label table, one thread per run
+    int total;
+    {
+        int v = lane < TY ? sm.rcnt[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(kFull, v, d);
+            if (lane >= d) v += u;
+        }
+        total = __shfl_sync(kFull, v, TY - 1);
+        if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
+        if (warp == 0 && lane == 0) sm.rbase[0] = 0;
+    }
     const int W = g.W, x0 = id.x0, y0 = id.y0;
-    for (int r = warp; r < TY; r += kWarps) {
-        const int k0 = row_run_base<TY>(sm, r, lane) + sm.wd[r][lane].pad;
-        int j = 0;
-        for_each_run_start<TY>(sm, r, lane, [&](int l) {
-            const int k = k0 + j++;
-            const uint32_t v = k < kRunCache ? sm.rc[k] : __ldg(Rt + k);
-            const int e = int(v >> 16);  // 1 + edge-list index, or 0
-            const int rr = int(v & 0x7FFFu);
-            int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
-            if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
-            sm.P[l >> 1] = lab | kTag;
-        });
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads) {
+        const uint32_t v = k < kRunCache ? reinterpret_cast<const uint32_t*>(sm.rc)[k] : __ldg(Rt + k);
+        const int e = int(v >> 16);  // 1 + edge-list index, or 0
+        const int rr = int(v & 0x7FFFu);
+        int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
+        if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
+        sm.lab[k] = lab;
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 2);
-    // stream the labels; every run-start entry of P now holds its tagged label
+
+    // 3. expand and stream every row
+    int4* buf = sm.rowbuf[warp];
     for (int r = warp; r < TY; r += kWarps) {
         const int y = y0 + r;
         if (y >= g.H) break;
         int32_t* orow = ob + size_t(y) * size_t(W) + x0;
-        const int rb = r * kTileW;
         if (VEC) {
-            // lane writes 4 consecutive pixels per step (512 B per warp store)
+            if (TMA) {  // the previous row's bulk store must have read the buffer
+                if (lane == 0) tma_wait_read_all();
+                __syncwarp();
+            }
+            const Word wd = sm.wd[r][lane];
+            const uint32_t m = wd.m, s = wd.s;
+            int idx = sm.rbase[r] + wd.pad - 1;  // run covering the word's bit 0 (if fg, not a start)
+            int c = ((m & 1u) && !(s & 1u)) ? sm.lab[idx] : 0;
+            const int lim = sm.rbase[TY] - 1;    // last valid run id (guards the speculative loads)
+#pragma unroll
+            for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
+                // branch-free: a 4-px group holds at most two run starts (starts
+                // are never adjacent), so its labels are c, L1 or L2 by the
+                // number of starts at or before each pixel
+                const uint32_t fm = (m >> (4 * q)) & 0xFu, fs = (s >> (4 * q)) & 0xFu;
+                const int L1 = sm.lab[min(idx + 1, lim)], L2 = sm.lab[min(idx + 2, lim)];
+                const uint32_t n0 = fs & 1u, n1 = __popc(fs & 3u), n2 = __popc(fs & 7u), n3 = __popc(fs);
+                const int a0 = n0 ? L1 : c;
+                const int a1 = n1 == 0 ? c : (n1 == 1 ? L1 : L2);
+                const int a2 = n2 == 0 ? c : (n2 == 1 ? L1 : L2);
+                const int a3 = n3 == 0 ? c : (n3 == 1 ? L1 : L2);
+                buf[swz(lane, q)] = make_int4((fm & 1u) ? a0 : 0, (fm & 2u) ? a1 : 0, (fm & 4u) ? a2 : 0,
+                                              (fm & 8u) ? a3 : 0);
+                c = a3;
+                idx += int(n3);
+            }
+            if (TMA) {
+                fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
+                __syncwarp();
+                if (lane == 0) tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
+            } else {
+                __syncwarp();
 #pragma unroll 2
-            for (int j = 0; j < kTileW / 128; ++j) {
-                const int x = 128 * j + 4 * lane;
-                if (x0 + x >= W) break;
-                const int w = x >> 5, sh = x & 31;
-                const Word wd = sm.wd[r][w];
-                const uint32_t fgn = (wd.m >> sh) & 0xFu;
-                int v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-                if (fgn) {
-                    const uint32_t stn = (wd.s >> sh) & 0xFu;
-                    int c = 0;
-                    if (fgn & 1u) {
-                        const uint32_t below = wd.s & (kFull >> (31 - sh));
-                        const int st = below ? ((w << 5) + 31 - __clz(below)) : wd.c;
-                        c = sm.P[(rb + st) >> 1];
-                    }
-                    const int pb = (rb + x) >> 1;  // P index of pixel x+1 / x+2 / x+3 starts
-                    v0 = c;
-                    if (stn & 2u) c = sm.P[pb];          // start at x+1: (rb+x+1)>>1 == pb
-                    v1 = c;
-                    if (stn & 4u) c = sm.P[pb + 1];      // start at x+2
-                    v2 = c;
-                    if (stn & 8u) c = sm.P[pb + 1];      // start at x+3: (rb+x+3)>>1 == pb+1
-                    v3 = c;
-                    v0 = (fgn & 1u) ? (v0 & 0x7FFFFFFF) : 0;
-                    v1 = (fgn & 2u) ? (v1 & 0x7FFFFFFF) : 0;
-                    v2 = (fgn & 4u) ? (v2 & 0x7FFFFFFF) : 0;
-                    v3 = (fgn & 8u) ? (v3 & 0x7FFFFFFF) : 0;
+                for (int j = 0; j < kTileW / 128; ++j) {
+                    const int x = 128 * j + 4 * lane;
+                    if (x0 + x >= W) break;
+                    const int4 v = buf[swz(4 * j + (lane >> 3), lane & 7)];
+                    st_stream_i4(orow + x, v.x, v.y, v.z, v.w);
                 }
-                st_stream_i4(orow + x, v0, v1, v2, v3);
+                __syncwarp();
             }
         } else {
+            // generic widths: lane writes pixel (k<<5) + lane of every word k
+            const int rb = sm.rbase[r];
             for (int k = 0; k < kWords; ++k) {
                 const int x = (k << 5) + lane;
                 if (x0 + x < W) {
-                    const uint32_t m = sm.wd[r][k].m;
+                    const Word wd = sm.wd[r][k];
                     int v = 0;
-                    if ((m >> lane) & 1u) {
-                        const int st = run_start_x(sm.wd[r], x);
-                        v = sm.P[(rb + st) >> 1] & 0x7FFFFFFF;
+                    if ((wd.m >> lane) & 1u) {
+                        const int run = rb + wd.pad + __popc(wd.s & (kFull >> (31 - lane))) - 1;
+                        v = sm.lab[run];
                     }
                     orow[x] = v;
                 }
@@ -1058,13 +1069,14 @@ __device__ __forceinline__ void k3_tile(TileSmem<TY>& sm, const Geom& g, unsigne
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 3);
 }
 
-template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, 4) k_link(Geom g, const uint32_t* __restrict__ bits,
+template <int TY, int CONN, bool VEC, bool TMA = false, int DBG = 0>
+__global__ void __launch_bounds__(kThreads, 3) k_link(Geom g, const uint32_t* __restrict__ bits,
                                                       const uint32_t* __restrict__ R,
                                                       const int32_t* __restrict__ F,
-                                                      int32_t* __restrict__ out, unsigned ntiles) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem<TY>& sm = *reinterpret_cast<TileSmem<TY>*>(smem_raw);
+                                                      int32_t* __restrict__ out, unsigned ntiles,
+                                                      const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    LinkSmem<TY>& sm = *reinterpret_cast<LinkSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
@@ -1072,14 +1084,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_link(Geom g, const uint32_t* __
     k3_prefetch<TY>(bits, R, F, g, t, warp, lane, a);
     while (true) {
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, b);
-        k3_tile<TY, CONN, VEC, DBG>(sm, g, t, a, R, F, out, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, t, a, R, F, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, a);
-        k3_tile<TY, CONN, VEC, DBG>(sm, g, t, b, R, F, out, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, t, b, R, F, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
     }
+    if (TMA && lane == 0) tma_wait_all();  // smem must outlive the bulk stores
 }
 
 }  // namespace ccl

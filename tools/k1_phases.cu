@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../paper_1708_08180_b200/csrc/ccl_kernels.cuh"
+#include <cudaTypedefs.h>
 
 #define CK(x)                                                                          \
     do {                                                                               \
@@ -200,23 +201,42 @@ int main(int argc, char** argv) {
     k1<<<grid1, ccl::kThreads, sm1>>>(img, g, bits, G, R, E, ntiles);
     ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
-    auto k3 = ccl::k_link<TY, 8, true, 0>;
-    auto k3s = ccl::k_link<TY, 8, true, 4>;
-    const size_t sm3 = sizeof(ccl::TileSmem<TY>);
+    auto k3 = ccl::k_link<TY, 8, true, true, 0>;
+    auto k3s = ccl::k_link<TY, 8, true, true, 4>;
+    const size_t sm3 = sizeof(ccl::LinkSmem<TY>);
+    CUtensorMap tmap;
+    {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        const cuuint64_t dims[3] = {32, cuuint64_t(W / 32), cuuint64_t(H)};
+        const cuuint64_t strides[2] = {128, cuuint64_t(W) * 4};
+        const cuuint32_t box[3] = {32, 32, 1}, es[3] = {1, 1, 1};
+        if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE))
+            printf("tensor map encode failed\n");
+    }
     CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     CK(cudaFuncSetAttribute(k3s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     for (int per_sm : {3, 4, 5}) {
         const int grid3 = std::min<int>(ntiles, sms * per_sm);
-        float us = timeit([&] { k3<<<grid3, ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles); }, flush, fb);
+        float us = timeit([&] { k3<<<grid3, ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
         printf("K3 x%d                              %8.1f us\n", per_sm, us);
+    }
+    {
+        auto k3z = ccl::k_link<TY, 8, true, true, 1>;
+        CK(cudaFuncSetAttribute(k3z, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+        float us = timeit([&] { k3z<<<std::min<int>(ntiles, sms * 3), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
+        printf("K3 x3, no expansion (stale rowbuf)  %8.1f us\n", us);
     }
     unsigned long long* st3;
     CK(cudaMalloc(&st3, size_t(ntiles) * 8 * 8));
     CK(cudaMemcpyToSymbol(ccl::g_k3_stamps, &st3, sizeof(st3)));
-    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles); }, flush, fb);
+    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
     printf("K3 + stamps x4                     %8.1f us\n", us3);
     CK(cudaMemcpy(hs.data(), st3, hs.size() * 8, cudaMemcpyDeviceToHost));
-    const char* n3[3] = {"load+row init", "run labels", "write"};
+    const char* n3[3] = {"row runs", "label table", "expand+write"};
     double a3[3] = {0}, t3 = 0;
     for (unsigned t = 0; t < ntiles; ++t)
         for (int k = 0; k < 3; ++k) a3[k] += double(hs[t * 8 + k + 1] - hs[t * 8 + k]);
