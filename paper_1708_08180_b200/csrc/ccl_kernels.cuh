@@ -663,10 +663,12 @@ __device__ __forceinline__ size_t tile_index(const Geom& g, int b, int ty, int t
 }
 
 // The horizontal boundary above tile (b, band >= 1, tx); one warp.
+constexpr int kPairsPerLane = 8;  // boundary pairs a lane contributes per round
+
 template <int TY, int CONN, bool NOUNION = false>
 __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
                                            const int32_t* E, int32_t* G, int b, int band, int tx,
-                                           Word (*s_w)[kWords]) {
+                                           Word (*s_w)[kWords], int2* pairs) {
     const int lane = threadIdx.x & 31;
     constexpr int RCAP = runs_per_tile_cap<TY>();
     const int x0 = tx * kTileW, y0 = band * TY;
@@ -722,34 +724,57 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     };
     const int W = g.W;
     unsigned long long last = ~0ull;
+    // Rounds: every lane turns up to kPairsPerLane of its events into root
+    // pairs in the warp's shared list; the list is then unioned with the pairs
+    // spread over all 32 lanes (a lane with many events no longer serialises
+    // the warp's union latency).
     while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
-        int a = -1, c = -1;
-        if (ev) {
-            const int x = (lane << 5) + __ffs(ev) - 1;
-            ev &= ev - 1;
-            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-            c = rec_root(__ldcg(Rup + run_idx(1, x)), W, x0, y0 - TY);
-        } else if (ne) {
-            const int x = (lane << 5) + __ffs(ne) - 1;
-            ne &= ne - 1;
-            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-            c = rec_root(__ldcg(Rup + run_idx(1, x + 1)), W, x0, y0 - TY);
-        } else if (nw) {
-            const int x = (lane << 5) + __ffs(nw) - 1;
-            nw &= nw - 1;
-            a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-            c = rec_root(__ldcg(Rup + run_idx(1, x - 1)), W, x0, y0 - TY);
-        } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
-            cnw = false;
-            a = __ldcg(E + t_lo * kEdgeCap + kEdgeLC);
-            c = __ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1);
-        } else if (cne) {  // (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
-            cne = false;
-            a = __ldcg(E + t_lo * kEdgeCap + kEdgeRC);
-            c = __ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1);
+        const int have = __popc(ev) + __popc(ne) + __popc(nw) + int(cnw) + int(cne);
+        const int take = min(have, kPairsPerLane);
+        int incl = take;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += u;
         }
-        CCL_ASSERT(a < 0 || (a < g.npx && c >= 0 && c < g.npx));
-        warp_union_pairs<NOUNION>(Gb, a, c, last);
+        const int total = __shfl_sync(kFull, incl, 31);
+        int pos = incl - take;
+        for (int e = 0; e < take; ++e) {
+            int a, c;
+            if (ev) {
+                const int x = (lane << 5) + __ffs(ev) - 1;
+                ev &= ev - 1;
+                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+                c = rec_root(__ldcg(Rup + run_idx(1, x)), W, x0, y0 - TY);
+            } else if (ne) {
+                const int x = (lane << 5) + __ffs(ne) - 1;
+                ne &= ne - 1;
+                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+                c = rec_root(__ldcg(Rup + run_idx(1, x + 1)), W, x0, y0 - TY);
+            } else if (nw) {
+                const int x = (lane << 5) + __ffs(nw) - 1;
+                nw &= nw - 1;
+                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
+                c = rec_root(__ldcg(Rup + run_idx(1, x - 1)), W, x0, y0 - TY);
+            } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
+                cnw = false;
+                a = __ldcg(E + t_lo * kEdgeCap + kEdgeLC);
+                c = __ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1);
+            } else {  // cne: (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
+                cne = false;
+                a = __ldcg(E + t_lo * kEdgeCap + kEdgeRC);
+                c = __ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1);
+            }
+            CCL_ASSERT(a >= 0 && a < g.npx && c >= 0 && c < g.npx);
+            pairs[pos++] = make_int2(a, c);
+        }
+        __syncwarp();
+        for (int base = 0; base < total; base += 32) {
+            const int i = base + lane;
+            const int2 pr = i < total ? pairs[i] : make_int2(-1, -1);
+            warp_union_pairs<NOUNION>(Gb, pr.x, pr.y, last);
+        }
+        __syncwarp();
     }
     __syncwarp();
 }
@@ -789,6 +814,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
                                                   const int32_t* __restrict__ E,
                                                   int32_t* __restrict__ G, long long n_h, long long n_v) {
     __shared__ Word s_w[8][2][kWords];
+    __shared__ int2 s_pairs[8][32 * kPairsPerLane];
     const int warp = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * 8 + warp;
     if (task < n_h) {
@@ -798,7 +824,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         t /= g.tiles_x;
         const int band = 1 + int(t % (g.tiles_y - 1));
         const int b = int(t / (g.tiles_y - 1));
-        boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp]);
+        boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp]);
     } else if (task < n_h + n_v) {
         if (DBG & 1) return;
         long long t = task - n_h;
