@@ -172,7 +172,8 @@ __device__ __forceinline__ void st_volatile(int32_t* p, int v) {
 }
 
 #ifdef CCL_STATS
-__device__ unsigned long long g_stat_unions = 0, g_stat_steps = 0;
+__device__ unsigned long long g_stat_unions = 0, g_stat_steps = 0, g_stat_finds = 0, g_stat_hops = 0,
+                              g_stat_maxhops = 0;
 #define CCL_STAT(v) atomicAdd(&(v), 1ull)
 #else
 #define CCL_STAT(v) ((void)0)
@@ -207,6 +208,10 @@ __device__ __forceinline__ int find_g(int32_t* G, int a) {
     }
     return a;
 }
+// (A two-pass full path compression here -- rewriting every visited node to
+// the root found through possibly stale L1 values -- lost unions under heavy
+// contention (percolation noise) and was dropped; halving stores only ever
+// write a grandparent read one step earlier.)
 
 __device__ __forceinline__ void union_g(int32_t* G, int a, int b) {
     CCL_STAT(g_stat_unions);
@@ -229,12 +234,23 @@ __device__ __forceinline__ void union_g(int32_t* G, int a, int b) {
 __device__ __forceinline__ int find_g_ro(const int32_t* G, int a) {
     int p = __ldg(G + a);
     CCL_LOOP_GUARD(fg);
+#ifdef CCL_STATS
+    unsigned long long hops = 0;
+    atomicAdd(&g_stat_finds, 1ull);
+#endif
     while (p != a) {
+#ifdef CCL_STATS
+        ++hops;
+#endif
         CCL_LOOP_TICK(fg);
         CCL_ASSERT(p >= 0 && p < a);
         a = p;
         p = __ldg(G + a);
     }
+#ifdef CCL_STATS
+    atomicAdd(&g_stat_hops, hops);
+    atomicMax(&g_stat_maxhops, hops);
+#endif
     return a;
 }
 
