@@ -151,7 +151,7 @@ int persistent_blocks(int which) {
     int sms = 0, b = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (which == 1)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads1,
                                                       smem_bytes_k1<TY>());
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC, true>, ccl::kThreads,
@@ -178,7 +178,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads, smem_bytes_k1<TY>(), s>>>(
+        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads1, smem_bytes_k1<TY>(), s>>>(
             img, g, bits, G, runs, E, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -50,6 +50,8 @@ constexpr int kTileW = 1024;   // pixels per tile row
 constexpr int kWords = 32;     // 32-bit mask words per tile row
 constexpr int kThreads = 256;  // threads per K1/K3 block
 constexpr int kWarps = kThreads / 32;
+constexpr int kThreads1 = 256;  // threads per K1 block (512 measured slower on texture, faster on noise)
+constexpr int kWarps1 = kThreads1 / 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
 
@@ -305,7 +307,7 @@ struct K1Smem {
     int32_t P[TY * kTileW / 2];    // parent over tile run ids (min-root forest)
     uint32_t flag[TY * kTileW / 64];  // run k is a root whose component touches a tile edge
     int32_t fpre[TY * kTileW / 64];   // exclusive prefix of popc(flag[])
-    int32_t wsum[kWarps];
+    int32_t wsum[kWarps1];
     int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
     int32_t rcnt[TY];              // runs per row
     int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
@@ -365,7 +367,7 @@ __device__ __forceinline__ void k3_stamp(unsigned t, int k) {
 
 template <int TY>
 struct ImgRegs {
-    uint4 v[TY / kWarps][2];
+    uint4 v[(TY + kWarps1 - 1) / kWarps1][2];
 };
 
 template <int TY>
@@ -377,8 +379,8 @@ __device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, u
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
 #pragma unroll
-    for (int i = 0; i < TY / kWarps; ++i) {
-        const int y = id.y0 + warp + i * kWarps;
+    for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
+        const int y = (warp + i * kWarps1 < TY) ? id.y0 + warp + i * kWarps1 : g.H;
         pf.v[i][0] = make_uint4(0, 0, 0, 0);
         pf.v[i][1] = make_uint4(0, 0, 0, 0);
         if (y < g.H) {
@@ -421,8 +423,9 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // Alg. 1 l.3-8: the tile's pixels -> foreground masks (out-of-image pixels
     // read as background, R5)
 #pragma unroll
-    for (int i = 0; i < TY / kWarps; ++i) {
-        const int r = warp + i * kWarps;
+    for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
+        const int r = warp + i * kWarps1;
+        if (r >= TY) break;  // warp-uniform
         const int y = id.y0 + r;
         uint32_t m = 0;
         if (VEC) {
@@ -454,7 +457,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
         k1_row_init<TY>(sm, r, lane, m);
     }
-    for (int i = tid; i < TY * kTileW / 64; i += kThreads) sm.flag[i] = 0;
+    for (int i = tid; i < TY * kTileW / 64; i += kThreads1) sm.flag[i] = 0;
     if (tid < TY) sm.lc[tid] = -1;
     else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
     __syncthreads();
@@ -472,8 +475,9 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         total = __shfl_sync(kFull, v, TY - 1);
         if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
         if (warp == 0 && lane == 0) sm.rbase[0] = 0;
-        for (int i = 0; i < TY / kWarps; ++i) {
-            const int r = warp + i * kWarps;
+        for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
+            const int r = warp + i * kWarps1;
+            if (r >= TY) break;  // warp-uniform
             const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
             const WordE w = sm.wd[r][lane];
             const int xb = lane << 5;
@@ -494,7 +498,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         }
     }
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads) sm.P[k] = k;
+    for (int k = tid; k < total; k += kThreads1) sm.P[k] = k;
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
     if (DBG & 1) {
@@ -509,7 +513,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // most two unions, found in O(1) from the masks: no fan-in serialisation.
     constexpr int D = CONN == 8 ? 1 : 0;
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads) {
+    for (int k = tid; k < total; k += kThreads1) {
         const int rsk = sm.rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
         const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
@@ -540,7 +544,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
     const bool left = x0 > 0, right = x0 + kTileW < W;
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads) {
+    for (int k = tid; k < total; k += kThreads1) {
         const int root = find_r_ro(sm.P, k);
         sm.P[k] = root;  // an ancestor: concurrent finds stay valid
         const int rsk = sm.rs[k];
@@ -568,7 +572,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // the roots, so the lists are deterministic)
     {
         constexpr int NW = TY * kTileW / 64;   // flag words
-        constexpr int PER = (NW + kThreads - 1) / kThreads;
+        constexpr int PER = (NW + kThreads1 - 1) / kThreads1;
         int loc[PER], sum = 0;
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -593,7 +597,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
             if (w < NW) sm.fpre[w] = run;
             run += loc[i];
         }
-        if (tid == kThreads - 1) E[size_t(t) * kEdgeCap] = wb + incl;  // list length
+        if (tid == kThreads1 - 1) E[size_t(t) * kEdgeCap] = wb + incl;  // list length
     }
     __syncthreads();
     // edge block header + column roots, per-run records for K3, the edge-root
@@ -609,7 +613,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
     int32_t* Et = Eh + kEdgeList;
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads) {
+    for (int k = tid; k < total; k += kThreads1) {
         const int root = sm.P[k];
         const int rr = sm.rs[root];  // row*1024 + x of the root run's start
         const uint32_t fw = sm.flag[root >> 5];
@@ -860,7 +864,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, 3) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+__global__ void __launch_bounds__(kThreads1, 3) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              int32_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
