@@ -7,7 +7,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <mutex>
 
 namespace {
@@ -126,6 +128,29 @@ bool encode_label_map(CUtensorMap* map, int32_t* out, const ccl::Geom& g) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel's blocks
+// may be scheduled while the previous kernel on the stream drains; the kernel
+// itself waits (griddepcontrol.wait) before touching its inputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = [] {
+        const char* v = std::getenv("CCL_PDL");
+        return v && v[0] == '0';
+    }();
+    cfg.attrs = attr;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 enum Stage { kK1 = 1, kK2 = 2, kK3 = 4, kAll = 7, kStripEdges = 8, kStripFinalize = 16 };
 
 // Strip-mode arguments (row-strip sharding, ccl_strip_local / _finalize).
@@ -188,12 +213,14 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
         const long long n_v = (long long)g.B * g.tiles_y * (g.tiles_x - 1);
         if (n_h + n_v > 0) {
-            ccl::k_boundary<TY, CONN><<<unsigned((n_h + n_v + 7) / 8), 256, 0, s>>>(g, bits, runs, E, G, n_h, n_v);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            e = launch_pdl(ccl::k_boundary<TY, CONN>, unsigned((n_h + n_v + 7) / 8), 256, 0, s, g,
+                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v);
+            if (e != cudaSuccess) return e;
         }
         const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-        ccl::k_resolve<TY><<<rblocks, 256, 0, s>>>(g, G, E, F, unsigned(ntiles));
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, (const int32_t*)G, (const int32_t*)E, F,
+                       unsigned(ntiles));
+        if (e != cudaSuccess) return e;
     }
     if (stages & kStripEdges) {
         // edge-root marks (Gs = out as scratch), boundary-row labels, slot reps
@@ -221,12 +248,14 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         CUtensorMap map;
         std::memset(&map, 0, sizeof(map));
         if (VEC && g.W % 32 == 0 && encode_label_map(&map, out, g))
-            ccl::k_link<TY, CONN, VEC, true><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out,
-                                                                              unsigned(ntiles), map);
+            e = launch_pdl(ccl::k_link<TY, CONN, VEC, true>, grid3, ccl::kThreads, smem, s, g,
+                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)F, out, unsigned(ntiles),
+                           map);
         else
-            ccl::k_link<TY, CONN, VEC, false><<<grid3, ccl::kThreads, smem, s>>>(g, bits, runs, F, out,
-                                                                               unsigned(ntiles), map);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            e = launch_pdl(ccl::k_link<TY, CONN, VEC, false>, grid3, ccl::kThreads, smem, s, g,
+                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)F, out, unsigned(ntiles),
+                           map);
+        if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

@@ -115,15 +115,31 @@ constexpr int kEdgeCap = 1152;
 constexpr int kEdgeCache = 32;  // resolved labels K3 prefetches per tile
 
 // ------------------------------------------------------------------ helpers
+// 4-bit mask of the nonzero bytes of w: the carry trick puts byte i's "nonzero"
+// bit at bit 8i+7; one multiply by 2^21+2^14+2^7+1 moves it to bit 28+i (the
+// 16 partial products land on distinct bits, so no carries) and >> 28 keeps
+// the nibble.
 __device__ __forceinline__ uint32_t nz4(uint32_t w) {
-    // 4-bit mask of the nonzero bytes of w
-    uint32_t t = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
-    return ((t >> 7) * 0x00204081u >> 21) & 0xFu;
+    const uint32_t t = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
+    return (t * 0x00204081u) >> 28;
 }
 
 __device__ __forceinline__ uint32_t nz16(uint4 v) {
-    return nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
+    uint32_t r = nz4(v.w);
+    r = (r << 4) + nz4(v.z);
+    r = (r << 4) + nz4(v.y);
+    return (r << 4) + nz4(v.x);
 }
+
+// Programmatic dependent launch (K2, resolve and K3 are launched with the
+// stream-serialisation attribute): a dependent grid is scheduled while its
+// predecessor drains (C3: 151 -> 145 us/step); wait blocks until the
+// predecessor has completed and its writes are visible (a no-op for a normal
+// launch).  No early launch_dependents trigger: letting the next grid's
+// blocks become resident before the predecessor's last blocks exit measured
+// slower (K3's blocks then hold shared memory the resolve / boundary blocks
+// need; 173 us with triggers at kernel entry, 148 with one in resolve).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Read-once image loads (no L1 allocation).  An L2 evict-first cache policy
 // on these loads measured slower for K1 and did not help K2 (profiles r01).
@@ -835,6 +851,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
                                                   int32_t* __restrict__ G, long long n_h, long long n_v) {
     __shared__ Word s_w[8][2][kWords];
     __shared__ int2 s_pairs[8][32 * kPairsPerLane];
+    pdl_wait();
     const int warp = threadIdx.x >> 5;
     const long long task = (long long)blockIdx.x * 8 + warp;
     if (task < n_h) {
@@ -900,6 +917,7 @@ template <int TY>
 __global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restrict__ G,
                                                  const int32_t* __restrict__ E,
                                                  int32_t* __restrict__ F, unsigned ntiles) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
     for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
@@ -1124,6 +1142,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_link(Geom g, const uint32_t* __
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     LinkSmem<TY>& sm = *reinterpret_cast<LinkSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_wait();
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
     LinkRegs<TY> a, b;
