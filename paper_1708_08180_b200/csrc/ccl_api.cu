@@ -211,14 +211,15 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         // K2: boundary unions (one warp per tile boundary), then resolve every
         // tile's edge-touching roots (one warp per tile)
         const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
-        const long long n_v = (long long)g.B * g.tiles_y * (g.tiles_x - 1);
+        const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
+                              (g.tiles_x - 1);
         if (n_h + n_v > 0) {
             e = launch_pdl(ccl::k_boundary<TY, CONN>, unsigned((n_h + n_v + 7) / 8), 256, 0, s, g,
                            (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v);
             if (e != cudaSuccess) return e;
         }
         const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-        e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, (const int32_t*)G, (const int32_t*)E, F,
+        e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, G, (const int32_t*)E, F,
                        unsigned(ntiles));
         if (e != cudaSuccess) return e;
     }

@@ -815,28 +815,31 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     __syncwarp();
 }
 
-// The vertical boundary left of tile (b, band, bx >= 1); one warp, lane = row.
+// The vertical boundary left of tile column bx >= 1 over kVBands = 32 / TY
+// consecutive tile bands starting at band0: one warp, lane = row (all 32 lanes
+// busy).  The NW / NE diagonal partners come from the lane above by shuffle;
+// lane 0's (the corner of a horizontal boundary) is covered by boundary_h.
+template <int TY>
+__host__ __device__ constexpr int v_bands() { return 32 / TY; }
+
 template <int TY, int CONN>
-__device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, int32_t* G, int b, int band,
+__device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, int32_t* G, int b, int band0,
                                            int bx) {
     const int lane = threadIdx.x & 31;
-    const int r = lane;
-    const size_t tr = tile_index(g, b, band, bx);  // tile right of the edge
-    const int32_t* Er = E + tr * kEdgeCap;
-    const int32_t* El = Er - kEdgeCap;              // tile left of the edge
+    const int band = band0 + lane / TY, r = lane % TY;
     int32_t* Gb = G + size_t(b) * size_t(g.npx);
-    int L = -1, Rr = -1, Lu = -1, Ru = -1;
-    if (r < TY && band * TY + r < g.H) {
+    int L = -1, Rr = -1;
+    if (band < g.tiles_y && band * TY + r < g.H) {
+        const int32_t* Er = E + tile_index(g, b, band, bx) * kEdgeCap;  // tile right of the edge
+        const int32_t* El = Er - kEdgeCap;                               // tile left of the edge
         L = __ldcg(El + kEdgeRC + r);   // root of (x0-1, y), or -1
         Rr = __ldcg(Er + kEdgeLC + r);  // root of (x0, y), or -1
-        if (CONN == 8 && r > 0 && (L >= 0 || Rr >= 0)) {
-            Lu = __ldcg(El + kEdgeRC + r - 1);
-            Ru = __ldcg(Er + kEdgeLC + r - 1);
-        }
     }
     unsigned long long last = ~0ull;
     warp_union_pairs(Gb, (L >= 0 && Rr >= 0) ? L : -1, Rr, last);        // W edge of (x0, y)
     if (CONN == 8) {
+        int Lu = __shfl_up_sync(kFull, L, 1), Ru = __shfl_up_sync(kFull, Rr, 1);
+        if (lane == 0) Lu = Ru = -1;
         warp_union_pairs(Gb, (Rr >= 0 && Lu >= 0) ? Rr : -1, Lu, last);  // NW of (x0, y)
         warp_union_pairs(Gb, (L >= 0 && Ru >= 0) ? L : -1, Ru, last);    // NE of (x0-1, y)
     }
@@ -867,9 +870,10 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         long long t = task - n_h;
         const int bx = 1 + int(t % (g.tiles_x - 1));
         t /= (g.tiles_x - 1);
-        const int band = int(t % g.tiles_y);
-        const int b = int(t / g.tiles_y);
-        boundary_v<TY, CONN>(g, E, G, b, band, bx);
+        const int groups = (g.tiles_y + v_bands<TY>() - 1) / v_bands<TY>();
+        const int band0 = int(t % groups) * v_bands<TY>();
+        const int b = int(t / groups);
+        boundary_v<TY, CONN>(g, E, G, b, band0, bx);
     }
 }
 
@@ -913,8 +917,17 @@ __global__ void __launch_bounds__(kThreads1, 3) k_local_merge(const uint8_t* __r
 // Boundary analysis, last step: every edge-touching local root of every tile
 // is resolved to its global root (find) once, all in parallel,
 // and 1 + root is stored in the tile's F list, so K3 needs no pointer chasing.
+//
+// Every edge root is owned by exactly one resolving thread (it is a local root
+// of one tile), and the long chains of the forest consist of edge roots only,
+// so the threads do concurrent pointer jumping: each repeatedly re-points ITS
+// node at the grandparent it reads (L2-coherent loads).  Other threads walking
+// through that node then skip ahead, so a chain of depth d is resolved in
+// ~log d rounds instead of d dependent loads (the read-only walk left the
+// kernel waiting on a few 30+-hop chains).  Entries only ever move to
+// ancestors, so the forest stays valid for later readers.
 template <int TY>
-__global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restrict__ G,
+__global__ void __launch_bounds__(256) k_resolve(Geom g, int32_t* __restrict__ G,
                                                  const int32_t* __restrict__ E,
                                                  int32_t* __restrict__ F, unsigned ntiles) {
     pdl_wait();
@@ -923,8 +936,23 @@ __global__ void __launch_bounds__(256) k_resolve(Geom g, const int32_t* __restri
     for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
         const int32_t* Et = E + size_t(t) * kEdgeCap;
         const int n = Et[0];
-        const int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
-        for (int i = lane; i < n; i += 32) F[size_t(t) * kEdgeCap + i] = find_g_ro(Gb, Et[kEdgeList + i]) + 1 + g.label_off;
+        int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
+        for (int i = lane; i < n; i += 32) {
+            const int x = Et[kEdgeList + i];
+            int p = __ldcg(Gb + x);
+            CCL_LOOP_GUARD(pj);
+            if (p != x) {
+                while (true) {
+                    CCL_LOOP_TICK(pj);
+                    const int gp = __ldcg(Gb + p);
+                    if (gp == p) break;
+                    CCL_ASSERT(gp < p);
+                    __stcg(Gb + x, gp);
+                    p = gp;
+                }
+            }
+            F[size_t(t) * kEdgeCap + i] = p + 1 + g.label_off;
+        }
     }
 }
 

@@ -152,7 +152,7 @@ int main(int argc, char** argv) {
     auto k1 = ccl::k_local_merge<TY, 8, true, 0>;
     const int grid1 = std::min<int>(ntiles, sms * 3);
     const size_t sm1 = sizeof(ccl::K1Smem<TY>);
-    const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)g.tiles_y * (g.tiles_x - 1);
+    const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) * (g.tiles_x - 1);
     const long long bh = (n_h + n_v + 7) / 8, bv = 0;
     auto time_k2 = [&](auto k2, const char* nm) {
         cudaEvent_t a, b;
