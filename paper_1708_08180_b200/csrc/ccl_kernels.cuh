@@ -604,8 +604,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         }
         if (lane == 31) sm.wsum[warp] = incl;
         __syncthreads();
-        int wb = 0;
-        for (int i = 0; i < warp; ++i) wb += sm.wsum[i];
+        const int wb = __reduce_add_sync(kFull, lane < warp ? sm.wsum[lane] : 0);
         int run = wb + incl - sum;
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -666,12 +665,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
 // of the tile rows next to a horizontal boundary and the column-root lists of
 // the tiles next to a vertical boundary -- so the only scattered accesses are
 // the union walks over the roots' parent entries in G.
-//
-// The unions run inside K1 (k_local_merge): a boundary is processed by the
-// block that finishes the SECOND of its two tiles (an arrival counter per
-// boundary), so the latency-bound global unions overlap the streaming local
-// merge of other tiles instead of forming a serial phase.  Reads of the
-// neighbour tile's outputs use ld.global.cg (L2, never a stale L1 line).
+// K1's outputs are read with ld.global.cg (L2).
 
 // Warp-cooperative union of a batch of root pairs: each lane holds at most one
 // pair (a, b) (a < 0: none).  Pairs already seen in this warp are dropped
@@ -845,8 +839,8 @@ __device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, int3
     }
 }
 
-// Standalone boundary analysis (all boundaries, one warp each); used when the
-// unions are not fused into K1 (profiling / the stage API's ablation path).
+// K2 boundary analysis: one warp per horizontal tile boundary (1024 px) or per
+// 32-row stretch of a vertical one; tasks are independent (lock-free unions).
 template <int TY, int CONN, int DBG = 0>
 __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
                                                   const uint32_t* __restrict__ R,
@@ -856,21 +850,22 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
     __shared__ int2 s_pairs[8][32 * kPairsPerLane];
     pdl_wait();
     const int warp = threadIdx.x >> 5;
-    const long long task = (long long)blockIdx.x * 8 + warp;
-    if (task < n_h) {
+    // (task counts are < 2^31: <= 2 per 16 x 1024 tile; 32-bit index math)
+    const unsigned task = blockIdx.x * 8u + unsigned(warp);
+    if (task < unsigned(n_h)) {
         if (DBG & 2) return;
-        long long t = task;
-        const int tx = int(t % g.tiles_x);
-        t /= g.tiles_x;
-        const int band = 1 + int(t % (g.tiles_y - 1));
-        const int b = int(t / (g.tiles_y - 1));
+        unsigned t = task;
+        const int tx = int(t % unsigned(g.tiles_x));
+        t /= unsigned(g.tiles_x);
+        const int band = 1 + int(t % unsigned(g.tiles_y - 1));
+        const int b = int(t / unsigned(g.tiles_y - 1));
         boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp]);
-    } else if (task < n_h + n_v) {
+    } else if (task < unsigned(n_h + n_v)) {
         if (DBG & 1) return;
-        long long t = task - n_h;
-        const int bx = 1 + int(t % (g.tiles_x - 1));
-        t /= (g.tiles_x - 1);
-        const int groups = (g.tiles_y + v_bands<TY>() - 1) / v_bands<TY>();
+        unsigned t = task - unsigned(n_h);
+        const int bx = 1 + int(t % unsigned(g.tiles_x - 1));
+        t /= unsigned(g.tiles_x - 1);
+        const unsigned groups = unsigned(g.tiles_y + v_bands<TY>() - 1) / v_bands<TY>();
         const int band0 = int(t % groups) * v_bands<TY>();
         const int b = int(t / groups);
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
