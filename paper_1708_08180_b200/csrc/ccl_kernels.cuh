@@ -1024,6 +1024,20 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// x | all lower bits of x within each 4-bit nibble (prefix OR per nibble)
+__device__ __forceinline__ uint32_t nibble_prefix_or(uint32_t x) {
+    x |= (x << 1) & 0xEEEEEEEEu;
+    return x | ((x << 2) & 0xCCCCCCCCu);
+}
+
+// x != 0 ? a : b as a predicated select (keeps the expansion loop branch-free)
+__device__ __forceinline__ int selp_nz(uint32_t x, int a, int b) {
+    int r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"(x));
+    return r;
+}
+
 // 16-byte slot of 4-px group q (0..255) of a row in the swizzled row buffer:
 // group q = 8*w + g (word w, group g within the word) lives at 8*w + (g ^ (w & 7)).
 __device__ __forceinline__ int swz(int w, int g) { return (w << 3) + (g ^ (w & 7)); }
@@ -1103,22 +1117,27 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, unsigne
             int idx = sm.rbase[r] + wd.pad - 1;  // run covering the word's bit 0 (if fg, not a start)
             int c = ((m & 1u) && !(s & 1u)) ? sm.lab[idx] : 0;
             const int lim = sm.rbase[TY] - 1;    // last valid run id (guards the speculative loads)
+            // A 4-px group holds at most two run starts (starts are never
+            // adjacent), so each pixel's label is 0, c (the run entering the
+            // group), L1 or L2 (the group's first / second new run).  2-bit
+            // code per pixel, built for the whole word at once: P1 / P2 = "at
+            // least one / two starts at or before this pixel within its group".
+            const uint32_t P1 = nibble_prefix_or(s);
+            const uint32_t P2 = nibble_prefix_or(s & ((P1 << 1) & 0xEEEEEEEEu));
+            const uint32_t Hi = m & P1;           // code 2 (L1) or 3 (L2)
+            const uint32_t Lo = m & (~P1 | P2);   // code 1 (c) or 3 (L2)
 #pragma unroll
             for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
-                // branch-free: a 4-px group holds at most two run starts (starts
-                // are never adjacent), so its labels are c, L1 or L2 by the
-                // number of starts at or before each pixel
-                const uint32_t fm = (m >> (4 * q)) & 0xFu, fs = (s >> (4 * q)) & 0xFu;
                 const int L1 = sm.lab[min(idx + 1, lim)], L2 = sm.lab[min(idx + 2, lim)];
-                const uint32_t n0 = fs & 1u, n1 = __popc(fs & 3u), n2 = __popc(fs & 7u), n3 = __popc(fs);
-                const int a0 = n0 ? L1 : c;
-                const int a1 = n1 == 0 ? c : (n1 == 1 ? L1 : L2);
-                const int a2 = n2 == 0 ? c : (n2 == 1 ? L1 : L2);
-                const int a3 = n3 == 0 ? c : (n3 == 1 ? L1 : L2);
-                buf[swz(lane, q)] = make_int4((fm & 1u) ? a0 : 0, (fm & 2u) ? a1 : 0, (fm & 4u) ? a2 : 0,
-                                              (fm & 8u) ? a3 : 0);
-                c = a3;
-                idx += int(n3);
+                int v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t bit = 1u << (4 * q + j);
+                    v[j] = selp_nz(Hi & bit, selp_nz(Lo & bit, L2, L1), selp_nz(Lo & bit, c, 0));
+                }
+                buf[swz(lane, q)] = make_int4(v[0], v[1], v[2], v[3]);
+                c = v[3];  // pixel 3 background => the next fg pixel starts a run
+                idx += __popc((s >> (4 * q)) & 0xFu);
             }
             if (TMA) {
                 fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
