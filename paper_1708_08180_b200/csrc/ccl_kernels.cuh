@@ -479,7 +479,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
 
-    // run lists: rs / re in raster order of the starts; P[k] = k
+    // run lists: rs / re in raster order of the starts, P[k] = k
     int total;
     {
         int v = lane < TY ? sm.rcnt[lane] : 0;
@@ -502,7 +502,9 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
             while (bits_) {
                 const int bit = __ffs(bits_) - 1;
                 bits_ &= bits_ - 1;
-                sm.rs[k++] = uint16_t((xb + bit) | (r << 10));
+                sm.rs[k] = uint16_t((xb + bit) | (r << 10));
+                sm.P[k] = k;
+                ++k;
             }
             k = rb + w.pad - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
             bits_ = w.e;
@@ -513,8 +515,6 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
             }
         }
     }
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) sm.P[k] = k;
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
     if (DBG & 1) {
@@ -953,28 +953,38 @@ __global__ void __launch_bounds__(256) k_resolve(Geom g, int32_t* __restrict__ G
 
 // ================================================================ K3: link
 // Final link (§2.3).  Per tile:
-//  1. row runs re-derived from the bit mask (start masks + run numbering only,
-//     no union-find);
+//  1. row runs re-derived from the bit mask (run numbering only, no
+//     union-find);
 //  2. one thread per run: final label = 1 + global root (K1's per-run record),
 //     or the boundary analysis' resolved label when the component touches a
 //     tile edge -> label table lab[run id];
-//  3. per tile row, every lane expands its own 32-px word into labels (the
-//     label changes only at run starts, so a 4-px group costs one test in the
-//     common case) into a per-warp shared-memory row buffer (XOR-swizzled:
-//     conflict-free 128-bit stores and loads), then the warp streams the row
-//     out with coalesced 128-bit evict-first stores (512 contiguous bytes per
-//     warp instruction).
+//  3. per tile row, every lane expands its own 32-px word into labels
+//     (branch-free, 4-px groups) into a per-warp shared-memory row buffer in
+//     the TMA 128-byte-swizzle layout, and one lane issues a bulk-tensor store
+//     of the 4 KB row.
+// The label table holds kLabCap runs; a tile with more runs (noise-like
+// content) is linked in row windows that each fit the table (54 KB of shared
+// memory per block).  3 blocks per SM: 4 (register-capped at 64) measured
+// 57 vs 54 us on C3 texture -- more concurrent row streams, lower DRAM
+// efficiency -- though faster on noise (121 vs 150 us); 2 and 1: 62 / 90 us.
 // Persistent like K1: the next tile's mask words, first run records and first
 // resolved labels are prefetched into registers while the current tile is
 // processed.
+constexpr int kLabCap = 4096;
+
+struct __align__(8) LWord {
+    uint32_t m;   // foreground mask
+    int32_t pad;  // run starts in the row before this word
+};
+
 template <int TY>
 struct __align__(1024) LinkSmem {
     // per-warp row of labels in the TMA SWIZZLE_128B layout: the 1024-px row is
     // a 32 x 128 B box (one 128-B row per 32-px word); 16-B unit q of word w
     // sits at w*128 + ((q ^ (w & 7)) * 16) -- also conflict-free for the lanes
     int4 rowbuf[kWarps][kTileW / 4];
-    Word wd[TY][kWords];             // .m mask, .s run starts, .pad runs before the word
-    int32_t lab[TY * kTileW / 2];    // final label of tile run k
+    LWord wd[TY][kWords];
+    int32_t lab[kLabCap];            // final label of tile run k (current row window)
     uint4 rc[kRunCache / 4];         // first run records of the tile (prefetched)
     int32_t fc[kEdgeCache];          // first resolved edge labels (prefetched)
     int32_t rcnt[TY];
@@ -1070,108 +1080,117 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, unsigne
             const int u = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += u;
         }
-        sm.wd[r][lane] = Word{m, s, 0, incl - n};
+        sm.wd[r][lane] = LWord{m, incl - n};
         if (lane == 31) sm.rcnt[r] = incl;
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 1);
-    // 2. label table, one thread per run
-    int total;
-    {
-        int v = lane < TY ? sm.rcnt[lane] : 0;
+    // run base of every row (lane r of every warp: v = first run id of row r+1)
+    int v = lane < TY ? sm.rcnt[lane] : 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int u = __shfl_up_sync(kFull, v, d);
-            if (lane >= d) v += u;
-        }
-        total = __shfl_sync(kFull, v, TY - 1);
-        if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
-        if (warp == 0 && lane == 0) sm.rbase[0] = 0;
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += u;
     }
+    if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
+    if (warp == 0 && lane == 0) sm.rbase[0] = 0;
     const int W = g.W, x0 = id.x0, y0 = id.y0;
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads) {
-        const uint32_t v = k < kRunCache ? reinterpret_cast<const uint32_t*>(sm.rc)[k] : __ldg(Rt + k);
-        const int e = int(v >> 16);  // 1 + edge-list index, or 0
-        const int rr = int(v & 0x7FFFu);
-        int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
-        if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
-        sm.lab[k] = lab;
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 2);
-
-    // 3. expand and stream every row
     int4* buf = sm.rowbuf[warp];
-    for (int r = warp; r < TY; r += kWarps) {
-        const int y = y0 + r;
-        if (y >= g.H) break;
-        int32_t* orow = ob + size_t(y) * size_t(W) + x0;
-        if (VEC) {
-            if (TMA) {  // the previous row's bulk store must have read the buffer
-                if (lane == 0) tma_wait_read_all();
-                __syncwarp();
-            }
-            const Word wd = sm.wd[r][lane];
-            const uint32_t m = wd.m, s = wd.s;
-            int idx = sm.rbase[r] + wd.pad - 1;  // run covering the word's bit 0 (if fg, not a start)
-            int c = ((m & 1u) && !(s & 1u)) ? sm.lab[idx] : 0;
-            const int lim = sm.rbase[TY] - 1;    // last valid run id (guards the speculative loads)
-            // A 4-px group holds at most two run starts (starts are never
-            // adjacent), so each pixel's label is 0, c (the run entering the
-            // group), L1 or L2 (the group's first / second new run).  2-bit
-            // code per pixel, built for the whole word at once: P1 / P2 = "at
-            // least one / two starts at or before this pixel within its group".
-            const uint32_t P1 = nibble_prefix_or(s);
-            const uint32_t P2 = nibble_prefix_or(s & ((P1 << 1) & 0xEEEEEEEEu));
-            const uint32_t Hi = m & P1;           // code 2 (L1) or 3 (L2)
-            const uint32_t Lo = m & (~P1 | P2);   // code 1 (c) or 3 (L2)
-#pragma unroll
-            for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
-                const int L1 = sm.lab[min(idx + 1, lim)], L2 = sm.lab[min(idx + 2, lim)];
-                int v[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t bit = 1u << (4 * q + j);
-                    v[j] = selp_nz(Hi & bit, selp_nz(Lo & bit, L2, L1), selp_nz(Lo & bit, c, 0));
+    // row windows [r0, r1) whose runs fit the label table (one window unless
+    // the tile has more than kLabCap runs)
+    int r0 = 0;
+    while (r0 < TY) {  // block-uniform
+        const int base = r0 > 0 ? __shfl_sync(kFull, v, r0 - 1) : 0;
+        const unsigned fit = __ballot_sync(kFull, lane >= r0 && lane < TY && v - base <= kLabCap);
+        const int r1 = 32 - __clz(fit);  // rows r0 .. r1-1 (v is monotone; >= 1 row: <= 512 runs per row)
+        const int end = __shfl_sync(kFull, v, r1 - 1);
+        // 2. label table, one thread per run of the window
+#pragma unroll 1
+        for (int k = base + tid; k < end; k += kThreads) {
+            const uint32_t rec = k < kRunCache ? reinterpret_cast<const uint32_t*>(sm.rc)[k] : __ldg(Rt + k);
+            const int e = int(rec >> 16);  // 1 + edge-list index, or 0
+            const int rr = int(rec & 0x7FFFu);
+            int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
+            if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
+            sm.lab[k - base] = lab;
+        }
+        __syncthreads();
+        if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 2);
+
+        // 3. expand and stream the window's rows
+        for (int r = r0 + warp; r < r1; r += kWarps) {
+            const int y = y0 + r;
+            if (y >= g.H) break;
+            int32_t* orow = ob + size_t(y) * size_t(W) + x0;
+            const int rb = sm.rbase[r] - base;
+            if (VEC) {
+                if (TMA) {  // the previous row's bulk store must have read the buffer
+                    if (lane == 0) tma_wait_read_all();
+                    __syncwarp();
                 }
-                buf[swz(lane, q)] = make_int4(v[0], v[1], v[2], v[3]);
-                c = v[3];  // pixel 3 background => the next fg pixel starts a run
-                idx += __popc((s >> (4 * q)) & 0xFu);
-            }
-            if (TMA) {
-                fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
-                __syncwarp();
-                if (lane == 0) tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
-            } else {
-                __syncwarp();
-#pragma unroll 2
-                for (int j = 0; j < kTileW / 128; ++j) {
-                    const int x = 128 * j + 4 * lane;
-                    if (x0 + x >= W) break;
-                    const int4 v = buf[swz(4 * j + (lane >> 3), lane & 7)];
-                    st_stream_i4(orow + x, v.x, v.y, v.z, v.w);
-                }
-                __syncwarp();
-            }
-        } else {
-            // generic widths: lane writes pixel (k<<5) + lane of every word k
-            const int rb = sm.rbase[r];
-            for (int k = 0; k < kWords; ++k) {
-                const int x = (k << 5) + lane;
-                if (x0 + x < W) {
-                    const Word wd = sm.wd[r][k];
-                    int v = 0;
-                    if ((wd.m >> lane) & 1u) {
-                        const int run = rb + wd.pad + __popc(wd.s & (kFull >> (31 - lane))) - 1;
-                        v = sm.lab[run];
+                const LWord wd = sm.wd[r][lane];
+                const uint32_t m = wd.m;
+                uint32_t pm = __shfl_up_sync(kFull, m, 1);
+                if (lane == 0) pm = 0;
+                const uint32_t s = m & ~((m << 1) | (pm >> 31));
+                int idx = rb + wd.pad - 1;           // run covering the word's bit 0 (if fg, not a start)
+                int c = ((m & 1u) && !(s & 1u)) ? sm.lab[idx] : 0;
+                const int lim = end - base - 1;      // last valid table entry (guards the speculative loads)
+                // A 4-px group holds at most two run starts (starts are never
+                // adjacent), so each pixel's label is 0, c (the run entering the
+                // group), L1 or L2 (the group's first / second new run).  2-bit
+                // code per pixel, built for the whole word at once: P1 / P2 = "at
+                // least one / two starts at or before this pixel within its group".
+                const uint32_t P1 = nibble_prefix_or(s);
+                const uint32_t P2 = nibble_prefix_or(s & ((P1 << 1) & 0xEEEEEEEEu));
+                const uint32_t Hi = m & P1;           // code 2 (L1) or 3 (L2)
+                const uint32_t Lo = m & (~P1 | P2);   // code 1 (c) or 3 (L2)
+#pragma unroll
+                for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
+                    const int L1 = sm.lab[min(idx + 1, lim)], L2 = sm.lab[min(idx + 2, lim)];
+                    int px[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t bit = 1u << (4 * q + j);
+                        px[j] = selp_nz(Hi & bit, selp_nz(Lo & bit, L2, L1), selp_nz(Lo & bit, c, 0));
                     }
-                    orow[x] = v;
+                    buf[swz(lane, q)] = make_int4(px[0], px[1], px[2], px[3]);
+                    c = px[3];  // pixel 3 background => the next fg pixel starts a run
+                    idx += __popc((s >> (4 * q)) & 0xFu);
+                }
+                if (TMA) {
+                    fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
+                    __syncwarp();
+                    if (lane == 0) tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
+                } else {
+                    __syncwarp();
+#pragma unroll 2
+                    for (int j = 0; j < kTileW / 128; ++j) {
+                        const int x = 128 * j + 4 * lane;
+                        if (x0 + x >= W) break;
+                        const int4 o = buf[swz(4 * j + (lane >> 3), lane & 7)];
+                        st_stream_i4(orow + x, o.x, o.y, o.z, o.w);
+                    }
+                    __syncwarp();
+                }
+            } else {
+                // generic widths: lane writes pixel (k<<5) + lane of every word k
+                for (int k = 0; k < kWords; ++k) {
+                    const int x = (k << 5) + lane;
+                    if (x0 + x < W) {
+                        const LWord wd = sm.wd[r][k];
+                        const uint32_t pm = k > 0 ? sm.wd[r][k - 1].m : 0u;
+                        const uint32_t s = wd.m & ~((wd.m << 1) | (pm >> 31));
+                        int o = 0;
+                        if ((wd.m >> lane) & 1u) o = sm.lab[rb + wd.pad + __popc(s & (kFull >> (31 - lane))) - 1];
+                        orow[x] = o;
+                    }
                 }
             }
         }
+        r0 = r1;
+        __syncthreads();  // the table (and, after the last window, all smem) is reused
     }
-    __syncthreads();  // smem is reused by the next tile
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 3);
 }
 
