@@ -320,10 +320,11 @@ struct K1Smem {
     WordE wd[TY][kWords];
     uint16_t rs[TY * kTileW / 2];  // run k: start x | row << 10
     uint16_t re[TY * kTileW / 2];  // run k: end x
-    int32_t P[TY * kTileW / 2];    // parent over tile run ids (min-root forest)
-    uint32_t flag[TY * kTileW / 64];  // run k is a root whose component touches a tile edge
-    int32_t fpre[TY * kTileW / 64];   // exclusive prefix of popc(flag[])
-    int32_t wsum[kWarps1];
+    // parent over tile run ids (min-root forest).  After the flatten, a root
+    // whose component touches a tile edge carries bit 31 and (1 + its
+    // edge-list index) << 16; the low 16 bits are always the parent id.
+    int32_t P[TY * kTileW / 2];
+    int32_t ecount;                // edge-list length
     int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
     int32_t rcnt[TY];              // runs per row
     int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
@@ -344,14 +345,16 @@ __device__ __forceinline__ int find_r(int32_t* P, int a) {
     return a;
 }
 
+// read-only find during the flatten: edge tags may be landing on roots, so
+// only the low 16 bits (the parent id) are followed
 __device__ __forceinline__ int find_r_ro(const int32_t* P, int a) {
     const volatile int32_t* V = P;
-    int p = V[a];
+    int p = V[a] & 0xFFFF;
     CCL_LOOP_GUARD(fro);
     while (p != a) {
         CCL_LOOP_TICK(fro);
         a = p;
-        p = V[a];
+        p = V[a] & 0xFFFF;
     }
     return a;
 }
@@ -473,9 +476,9 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
         k1_row_init<TY>(sm, r, lane, m);
     }
-    for (int i = tid; i < TY * kTileW / 64; i += kThreads1) sm.flag[i] = 0;
     if (tid < TY) sm.lc[tid] = -1;
     else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
+    else if (tid == 2 * TY) sm.ecount = 0;
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
 
@@ -549,9 +552,15 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
     // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
-    // index conversion): every run points at its root; the roots of top /
-    // bottom row runs and of left / right column pixels are flagged and the
-    // column pixels' roots recorded for the boundary analysis.
+    // index conversion): every run points at its root; the first run to find
+    // that its root's component touches a tile edge (top / bottom row run,
+    // left / right column pixel) claims the root (bit 31), appends it to the
+    // tile's edge-root list, writes its global parent entry and tags the root
+    // with 1 + its list index (list order = claim order: any bijection works,
+    // the labels do not depend on it).  The global parent entries G[r] = r
+    // are written as whole 32-byte sectors (identity for the 8 pixels: no
+    // other entry of G is ever read) so the boundary analysis' atomics and
+    // loads hit fully valid L2 sectors instead of filling from DRAM.
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     // rows that border another tile (or, in strip mode, another strip)
@@ -559,85 +568,23 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     const bool top = y0 > 0 || g.force_top;
     const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
     const bool left = x0 > 0, right = x0 + kTileW < W;
+    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
+    int32_t* Eh = E + size_t(t) * kEdgeCap;
+    int32_t* Et = Eh + kEdgeList;
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int root = find_r_ro(sm.P, k);
-        sm.P[k] = root;  // an ancestor: concurrent finds stay valid
+        if (root != k) sm.P[k] = root;  // an ancestor: concurrent finds stay valid
         const int rsk = sm.rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
         const bool hrow = (r == 0 && top) || (r == last_row && bottom);
         const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
         if (hrow || lc || rc) {
-            atomicOr(&sm.flag[root >> 5], 1u << (root & 31));
-            if (lc || rc) {
-                const int rr = sm.rs[root];
-                const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
-                if (lc) sm.lc[r] = gr;
-                if (rc) sm.rc[r] = gr;
-            }
-        }
-    }
-    if (DBG & 2) {
-        __syncthreads();
-        __syncthreads();
-        return;
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
-    // edge-root list order: exclusive prefix of the flag bits (raster order of
-    // the roots, so the lists are deterministic)
-    {
-        constexpr int NW = TY * kTileW / 64;   // flag words
-        constexpr int PER = (NW + kThreads1 - 1) / kThreads1;
-        int loc[PER], sum = 0;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int w = tid * PER + i;
-            loc[i] = w < NW ? __popc(sm.flag[w]) : 0;
-            sum += loc[i];
-        }
-        int incl = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int u = __shfl_up_sync(kFull, incl, d);
-            if (lane >= d) incl += u;
-        }
-        if (lane == 31) sm.wsum[warp] = incl;
-        __syncthreads();
-        const int wb = __reduce_add_sync(kFull, lane < warp ? sm.wsum[lane] : 0);
-        int run = wb + incl - sum;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int w = tid * PER + i;
-            if (w < NW) sm.fpre[w] = run;
-            run += loc[i];
-        }
-        if (tid == kThreads1 - 1) E[size_t(t) * kEdgeCap] = wb + incl;  // list length
-    }
-    __syncthreads();
-    // edge block header + column roots, per-run records for K3, the edge-root
-    // list, and the global parent entries G[root] = root of the edge roots.
-    // Those are written as whole 32-byte sectors (identity for the 8 pixels:
-    // no other entry of G is ever read) so the boundary analysis' atomics and
-    // loads hit fully valid L2 sectors instead of filling from DRAM.
-    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
-    int32_t* Eh = E + size_t(t) * kEdgeCap;
-    if (tid == 0) Eh[1] = sm.rbase[min(TY, g.H - y0) - 1];  // first run of the last valid row
-    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
-    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
-    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
-    int32_t* Et = Eh + kEdgeList;
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
-        const int root = sm.P[k];
-        const int rr = sm.rs[root];  // row*1024 + x of the root run's start
-        const uint32_t fw = sm.flag[root >> 5];
-        uint32_t rec = uint32_t(rr);
-        if ((fw >> (root & 31)) & 1u) {
-            const int idx = sm.fpre[root >> 5] + __popc(fw & ((1u << (root & 31)) - 1u));
-            rec |= uint32_t(idx + 1) << 16;
-            if (k == root) {
-                const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+            const int rr = sm.rs[root];
+            const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+            if (!(atomicOr(&sm.P[root], int(0x80000000u)) & int(0x80000000u))) {
+                const int idx = atomicAdd(&sm.ecount, 1);
+                sm.P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
                 Et[idx] = gr;
                 if ((g.npx & 7) == 0) {
                     // whole sector, identity: harmless for the 7 neighbours
@@ -651,8 +598,30 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
                     Gb[gr] = gr;
                 }
             }
+            if (lc) sm.lc[r] = gr;
+            if (rc) sm.rc[r] = gr;
         }
-        Rt[k] = rec;
+    }
+    if (DBG & 2) {
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
+    // edge block header + column roots, and the per-run records for K3 / K2
+    if (tid == 0) {
+        Eh[0] = sm.ecount;
+        Eh[1] = sm.rbase[last_row];  // first run of the last valid row
+    }
+    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
+    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
+    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int root = sm.P[k] & 0xFFFF;
+        const int tag = (sm.P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
+        Rt[k] = uint32_t(sm.rs[root]) | (uint32_t(tag) << 16);
     }
     __syncthreads();  // smem is reused by the next tile
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
