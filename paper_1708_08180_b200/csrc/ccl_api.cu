@@ -24,8 +24,8 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes;
-    size_t total() const { return G_bytes + bits_bytes + runs_bytes + 2 * edge_bytes; }
+    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, k1x_bytes;
+    size_t total() const { return G_bytes + bits_bytes + runs_bytes + 2 * edge_bytes + k1x_bytes; }
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -65,6 +65,12 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     // for the most tiles any config makes (tile_rows = 8)
     const size_t tiles8 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 7) / 8);
     p.edge_bytes = align_up(tiles8 * ccl::kEdgeCap * sizeof(int32_t));
+    // K1 scratch slots for tiles over the shared-memory run capacity (one per
+    // K1 block; tile_rows = 8 never overflows), sized for the larger need
+    const size_t tiles16 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 15) / 16);
+    const size_t tiles32 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 31) / 32);
+    p.k1x_bytes = align_up(std::max(std::min(tiles16, size_t(ccl::k1x_slots<16>())) * ccl::k1x_slot_bytes<16>(),
+                                    std::min(tiles32, size_t(ccl::k1x_slots<32>())) * ccl::k1x_slot_bytes<32>()));
     return CCL_OK;
 }
 
@@ -200,11 +206,13 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     if (ntiles == 0) return cudaSuccess;
     const size_t smem = smem_bytes<TY>();
     // persistent K1/K3: one wave of resident blocks walks all tiles
-    const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
+    const unsigned grid1 = unsigned(std::min<long long>(
+        std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)), ccl::k1x_slots<TY>()));
+    void* k1x = reinterpret_cast<char*>(F) + p.edge_bytes;
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
         ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads1, smem_bytes_k1<TY>(), s>>>(
-            img, g, bits, G, runs, E, unsigned(ntiles));
+            img, g, bits, G, runs, E, k1x, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {

@@ -315,15 +315,27 @@ struct __align__(16) WordE {
     int32_t pad;   // number of run starts in the row before this word
 };
 
+// Run lists of a tile live in shared memory up to k1_cap runs (natural
+// images: a few hundred; i.i.d. noise at density 1/2: ~4096), which keeps the
+// block at ~55 KB -- 4 blocks (32 warps) per SM.  A tile with more runs
+// (period-2 stripes, checkerboards: up to TY*512) keeps them in the block's
+// slot of a global scratch area instead (same code, L2-resident).
+template <int TY>
+__host__ __device__ constexpr int k1_cap() { return TY * kTileW / 2 < 5632 ? TY * kTileW / 2 : 5632; }
+template <int TY>
+__host__ __device__ constexpr size_t k1x_slot_bytes() { return size_t(TY) * (kTileW / 2) * 8; }
+template <int TY>
+__host__ __device__ constexpr int k1x_slots() { return TY > 16 ? 512 : 1024; }  // = max K1 grid
+
 template <int TY>
 struct K1Smem {
     WordE wd[TY][kWords];
-    uint16_t rs[TY * kTileW / 2];  // run k: start x | row << 10
-    uint16_t re[TY * kTileW / 2];  // run k: end x
+    uint16_t rs[k1_cap<TY>()];  // run k: start x | row << 10
+    uint16_t re[k1_cap<TY>()];  // run k: end x
     // parent over tile run ids (min-root forest).  After the flatten, a root
     // whose component touches a tile edge carries bit 31 and (1 + its
     // edge-list index) << 16; the low 16 bits are always the parent id.
-    int32_t P[TY * kTileW / 2];
+    int32_t P[k1_cap<TY>()];
     int32_t ecount;                // edge-list length
     int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
     int32_t rcnt[TY];              // runs per row
@@ -429,10 +441,152 @@ __device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uin
     if (lane == 31) sm.rcnt[r] = incl;
 }
 
+// K1 from the run lists on: rs / re / P are the block's shared arrays or, for
+// a tile over k1_cap runs, its global scratch slot.
+template <int TY, int CONN, int DBG>
+__device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ rs, uint16_t* __restrict__ re,
+                                        int32_t* P, const Geom& g, unsigned t, const TileId& id, int v,
+                                        int total, int32_t* G, uint32_t* R, int32_t* E, int warp, int lane) {
+    const int tid = threadIdx.x;
+    // run lists: rs / re in raster order of the starts, P[k] = k
+    {
+        for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
+            const int r = warp + i * kWarps1;
+            if (r >= TY) break;  // warp-uniform
+            const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
+            const WordE w = sm.wd[r][lane];
+            const int xb = lane << 5;
+            int k = rb + w.pad;
+            uint32_t bits_ = w.s;
+            while (bits_) {
+                const int bit = __ffs(bits_) - 1;
+                bits_ &= bits_ - 1;
+                rs[k] = uint16_t((xb + bit) | (r << 10));
+                P[k] = k;
+                ++k;
+            }
+            k = rb + w.pad - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
+            bits_ = w.e;
+            while (bits_) {
+                const int bit = __ffs(bits_) - 1;
+                bits_ &= bits_ - 1;
+                re[k++] = uint16_t(xb + bit);
+            }
+        }
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
+    if (DBG & 1) {
+        __syncthreads();
+        return;
+    }
+
+    // local UF.  The adjacencies between two rows form a monotone staircase of
+    // run pairs; every pair is (k, first upper neighbour of k) or (first lower
+    // neighbour of j, j) -- if j is the 2nd+ upper neighbour of k, j starts
+    // right of k's start, so it cannot reach k-1.  Each run therefore does at
+    // most two unions, found in O(1) from the masks: no fan-in serialisation.
+    constexpr int D = CONN == 8 ? 1 : 0;
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        if (r > 0) {  // first run of row r-1 touching [p, q]
+            const WordE u = sm.wd[r - 1][p >> 5];
+            const int open = (u.m & 1u) && !(u.s & 1u);
+            const int j = sm.rbase[r - 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            if (j < sm.rbase[r] && (rs[j] & 1023) <= q) union_r(P, k, j);
+        }
+        if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
+            const WordE u = sm.wd[r + 1][p >> 5];
+            const int open = (u.m & 1u) && !(u.s & 1u);
+            const int j = sm.rbase[r + 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            if (j < sm.rbase[r + 2] && (rs[j] & 1023) <= q) union_r(P, j, k);
+        }
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
+    // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
+    // index conversion): every run points at its root; the first run to find
+    // that its root's component touches a tile edge (top / bottom row run,
+    // left / right column pixel) claims the root (bit 31), appends it to the
+    // tile's edge-root list, writes its global parent entry and tags the root
+    // with 1 + its list index (list order = claim order: any bijection works,
+    // the labels do not depend on it).  The global parent entries G[r] = r
+    // are written as whole 32-byte sectors (identity for the 8 pixels: no
+    // other entry of G is ever read) so the boundary analysis' atomics and
+    // loads hit fully valid L2 sectors instead of filling from DRAM.
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
+    const int W = g.W, x0 = id.x0, y0 = id.y0;
+    // rows that border another tile (or, in strip mode, another strip)
+    const int last_row = min(TY, g.H - y0) - 1;
+    const bool top = y0 > 0 || g.force_top;
+    const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
+    const bool left = x0 > 0, right = x0 + kTileW < W;
+    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
+    int32_t* Eh = E + size_t(t) * kEdgeCap;
+    int32_t* Et = Eh + kEdgeList;
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int root = find_r_ro(P, k);
+        if (root != k) P[k] = root;  // an ancestor: concurrent finds stay valid
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const bool hrow = (r == 0 && top) || (r == last_row && bottom);
+        const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
+        if (hrow || lc || rc) {
+            const int rr = rs[root];
+            const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
+            if (!(atomicOr(&P[root], int(0x80000000u)) & int(0x80000000u))) {
+                const int idx = atomicAdd(&sm.ecount, 1);
+                P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
+                Et[idx] = gr;
+                if ((g.npx & 7) == 0) {
+                    // whole sector, identity: harmless for the 7 neighbours
+                    // (every root entry is still its own index during K1, all
+                    // other entries are never read); images are sector-aligned
+                    const int base = gr & ~7;
+                    int4* sec = reinterpret_cast<int4*>(Gb + base);
+                    sec[0] = make_int4(base, base + 1, base + 2, base + 3);
+                    sec[1] = make_int4(base + 4, base + 5, base + 6, base + 7);
+                } else {
+                    Gb[gr] = gr;
+                }
+            }
+            if (lc) sm.lc[r] = gr;
+            if (rc) sm.rc[r] = gr;
+        }
+    }
+    if (DBG & 2) {
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
+    // edge block header + column roots, and the per-run records for K3 / K2
+    if (tid == 0) {
+        Eh[0] = sm.ecount;
+        Eh[1] = sm.rbase[last_row];  // first run of the last valid row
+    }
+    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
+    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
+    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int root = P[k] & 0xFFFF;
+        const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
+        Rt[k] = uint32_t(rs[root]) | (uint32_t(tag) << 16);
+    }
+    __syncthreads();  // smem is reused by the next tile
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
+}
+
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
                                         const ImgRegs<TY>& cur, uint32_t* bits, int32_t* G,
-                                        uint32_t* R, int32_t* E, int warp, int lane) {
+                                        uint32_t* R, int32_t* E, void* k1x, int warp, int lane) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
@@ -482,149 +636,24 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
 
-    // run lists: rs / re in raster order of the starts, P[k] = k
-    int total;
-    {
-        int v = lane < TY ? sm.rcnt[lane] : 0;
+    // run numbering: v (lane r) = first run id of row r+1
+    int v = lane < TY ? sm.rcnt[lane] : 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int u = __shfl_up_sync(kFull, v, d);
-            if (lane >= d) v += u;
-        }
-        total = __shfl_sync(kFull, v, TY - 1);
-        if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
-        if (warp == 0 && lane == 0) sm.rbase[0] = 0;
-        for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
-            const int r = warp + i * kWarps1;
-            if (r >= TY) break;  // warp-uniform
-            const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
-            const WordE w = sm.wd[r][lane];
-            const int xb = lane << 5;
-            int k = rb + w.pad;
-            uint32_t bits_ = w.s;
-            while (bits_) {
-                const int bit = __ffs(bits_) - 1;
-                bits_ &= bits_ - 1;
-                sm.rs[k] = uint16_t((xb + bit) | (r << 10));
-                sm.P[k] = k;
-                ++k;
-            }
-            k = rb + w.pad - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
-            bits_ = w.e;
-            while (bits_) {
-                const int bit = __ffs(bits_) - 1;
-                bits_ &= bits_ - 1;
-                sm.re[k++] = uint16_t(xb + bit);
-            }
-        }
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += u;
     }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
-    if (DBG & 1) {
-        __syncthreads();
-        return;
+    const int total = __shfl_sync(kFull, v, TY - 1);  // block-uniform
+    if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
+    if (warp == 0 && lane == 0) sm.rbase[0] = 0;
+    if (total <= k1_cap<TY>()) {
+        k1_runs<TY, CONN, DBG>(sm, sm.rs, sm.re, sm.P, g, t, id, v, total, G, R, E, warp, lane);
+    } else {
+        char* slot = static_cast<char*>(k1x) + size_t(blockIdx.x) * k1x_slot_bytes<TY>();
+        constexpr int N = TY * kTileW / 2;
+        k1_runs<TY, CONN, DBG>(sm, reinterpret_cast<uint16_t*>(slot), reinterpret_cast<uint16_t*>(slot) + N,
+                               reinterpret_cast<int32_t*>(slot + 4 * N), g, t, id, v, total, G, R, E, warp, lane);
     }
-
-    // local UF.  The adjacencies between two rows form a monotone staircase of
-    // run pairs; every pair is (k, first upper neighbour of k) or (first lower
-    // neighbour of j, j) -- if j is the 2nd+ upper neighbour of k, j starts
-    // right of k's start, so it cannot reach k-1.  Each run therefore does at
-    // most two unions, found in O(1) from the masks: no fan-in serialisation.
-    constexpr int D = CONN == 8 ? 1 : 0;
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
-        const int rsk = sm.rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
-        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        if (r > 0) {  // first run of row r-1 touching [p, q]
-            const WordE u = sm.wd[r - 1][p >> 5];
-            const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = sm.rbase[r - 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r] && (sm.rs[j] & 1023) <= q) union_r(sm.P, k, j);
-        }
-        if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
-            const WordE u = sm.wd[r + 1][p >> 5];
-            const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = sm.rbase[r + 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r + 2] && (sm.rs[j] & 1023) <= q) union_r(sm.P, j, k);
-        }
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
-    // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
-    // index conversion): every run points at its root; the first run to find
-    // that its root's component touches a tile edge (top / bottom row run,
-    // left / right column pixel) claims the root (bit 31), appends it to the
-    // tile's edge-root list, writes its global parent entry and tags the root
-    // with 1 + its list index (list order = claim order: any bijection works,
-    // the labels do not depend on it).  The global parent entries G[r] = r
-    // are written as whole 32-byte sectors (identity for the 8 pixels: no
-    // other entry of G is ever read) so the boundary analysis' atomics and
-    // loads hit fully valid L2 sectors instead of filling from DRAM.
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
-    const int W = g.W, x0 = id.x0, y0 = id.y0;
-    // rows that border another tile (or, in strip mode, another strip)
-    const int last_row = min(TY, g.H - y0) - 1;
-    const bool top = y0 > 0 || g.force_top;
-    const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
-    const bool left = x0 > 0, right = x0 + kTileW < W;
-    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
-    int32_t* Eh = E + size_t(t) * kEdgeCap;
-    int32_t* Et = Eh + kEdgeList;
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
-        const int root = find_r_ro(sm.P, k);
-        if (root != k) sm.P[k] = root;  // an ancestor: concurrent finds stay valid
-        const int rsk = sm.rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = sm.re[k];
-        const bool hrow = (r == 0 && top) || (r == last_row && bottom);
-        const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
-        if (hrow || lc || rc) {
-            const int rr = sm.rs[root];
-            const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
-            if (!(atomicOr(&sm.P[root], int(0x80000000u)) & int(0x80000000u))) {
-                const int idx = atomicAdd(&sm.ecount, 1);
-                sm.P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
-                Et[idx] = gr;
-                if ((g.npx & 7) == 0) {
-                    // whole sector, identity: harmless for the 7 neighbours
-                    // (every root entry is still its own index during K1, all
-                    // other entries are never read); images are sector-aligned
-                    const int base = gr & ~7;
-                    int4* sec = reinterpret_cast<int4*>(Gb + base);
-                    sec[0] = make_int4(base, base + 1, base + 2, base + 3);
-                    sec[1] = make_int4(base + 4, base + 5, base + 6, base + 7);
-                } else {
-                    Gb[gr] = gr;
-                }
-            }
-            if (lc) sm.lc[r] = gr;
-            if (rc) sm.rc[r] = gr;
-        }
-    }
-    if (DBG & 2) {
-        __syncthreads();
-        __syncthreads();
-        return;
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
-    // edge block header + column roots, and the per-run records for K3 / K2
-    if (tid == 0) {
-        Eh[0] = sm.ecount;
-        Eh[1] = sm.rbase[last_row];  // first run of the last valid row
-    }
-    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
-    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
-    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
-#pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
-        const int root = sm.P[k] & 0xFFFF;
-        const int tag = (sm.P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
-        Rt[k] = uint32_t(sm.rs[root]) | (uint32_t(tag) << 16);
-    }
-    __syncthreads();  // smem is reused by the next tile
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
 }
 
 // ============================================================ K2: boundary
@@ -849,12 +878,12 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads1, 3) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+__global__ void __launch_bounds__(kThreads1, 4) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              int32_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
                                                              int32_t* __restrict__ E,
-                                                             unsigned ntiles) {
+                                                             void* __restrict__ k1x, unsigned ntiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem<TY>& sm = *reinterpret_cast<K1Smem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -867,11 +896,11 @@ __global__ void __launch_bounds__(kThreads1, 3) k_local_merge(const uint8_t* __r
     if (PF) k1_prefetch<TY>(img, g, t, warp, lane, a);
     while (true) {
         if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, b);
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, bits, G, R, E, warp, lane);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, bits, G, R, E, k1x, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
         if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, a);
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, b, bits, G, R, E, warp, lane);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, b, bits, G, R, E, k1x, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
     }

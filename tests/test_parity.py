@@ -187,6 +187,24 @@ def test_config_independence(ccl):
             assert_same(gpu_label(ccl, img, conn, tile_rows=ty), ref, f"tile_rows={ty}")
 
 
+@pytest.mark.parametrize("conn", CONNS)
+def test_run_dense_tiles_global_scratch(ccl, conn):
+    # Tiles with more runs than K1's shared-memory capacity (5632 per tile:
+    # period-2 stripes / checkerboards reach TY*512) take the global-scratch
+    # path; mixed with ordinary tiles in one image and one batch.
+    H, W = 100, 3000
+    img = synth.texture(H, W, seed=21)
+    img[:, 1024:2048] = synth.stripes(H, 1024, period=2)      # 512 runs per row
+    img[40:72, 2048:3000] = synth.checkerboard(32, 952)       # 4-conn: 476 per row
+    img[0:16, 0:1024] = synth.stripes(16, 1024, period=2, vertical=False)
+    for ty in (8, 16, 32):
+        assert_same(gpu_label(ccl, img, conn, tile_rows=ty), oracle.label_bfs(img, conn), f"ty={ty}")
+    batch = np.stack([img, synth.checkerboard(H, W), synth.noise(H, W, 0.5, seed=5)])
+    import torch
+    got = ccl.label(torch.from_numpy(batch).cuda(), conn).cpu().numpy()
+    assert_same(got, oracle.label_bfs_batched(batch, conn), "batch")
+
+
 def test_determinism_repeated_runs(ccl):
     # byte-identical across repeated racy runs
     import torch

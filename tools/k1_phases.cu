@@ -10,6 +10,7 @@
 
 #include "../paper_1708_08180_b200/csrc/ccl_kernels.cuh"
 #include <cudaTypedefs.h>
+static void* g_k1x = nullptr;  // K1 overflow scratch
 
 #define CK(x)                                                                          \
     do {                                                                               \
@@ -60,7 +61,7 @@ void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, i
     auto k = ccl::k_local_merge<TY, CONN, true, DBG>;
     size_t smem = sizeof(ccl::K1Smem<TY>);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    float us = timeit([&] { k<<<grid, ccl::kThreads1, smem>>>(img, g, bits, G, R, E, ntiles); }, flush, fb);
+    float us = timeit([&] { k<<<grid, ccl::kThreads1, smem>>>(img, g, bits, G, R, E, g_k1x, ntiles); }, flush, fb);
     printf("%-34s grid %6d  %8.1f us\n", name, grid, us);
 }
 
@@ -93,6 +94,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&E, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
     CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
     CK(cudaMalloc(&flush, fb));
+    CK(cudaMalloc(&g_k1x, size_t(1024) * ccl::k1x_slot_bytes<32>()));
     unsigned* sink;
     CK(cudaMalloc(&sink, 64));
     CK(cudaMemcpy(img, h.data(), n, cudaMemcpyHostToDevice));
@@ -161,7 +163,7 @@ int main(int argc, char** argv) {
         float tot2 = 0;
         for (int i = 0; i < 23; ++i) {
             CK(cudaMemsetAsync(flush, i, fb));
-            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, ntiles);
+            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
             CK(cudaEventRecord(a));
             k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
             CK(cudaEventRecord(b));
@@ -178,7 +180,7 @@ int main(int argc, char** argv) {
     time_k2(ccl::k_boundary<TY, 8, 3>, "K2 empty (launch)");
     time_k2(ccl::k_boundary<TY, 8, 5>, "K2 horizontal, no unions");
     {
-        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, ntiles);
+        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         float us = timeit([&] { ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles); }, flush, fb);
         printf("%-34s %8.1f us\n", "K2b resolve", us);
@@ -189,7 +191,7 @@ int main(int argc, char** argv) {
         unsigned long long z = 0, u, st;
         CK(cudaMemcpyToSymbol(ccl::g_stat_unions, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_steps, &z, 8));
-        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, ntiles);
+        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpyFromSymbol(&u, ccl::g_stat_unions, 8));
@@ -208,7 +210,7 @@ int main(int argc, char** argv) {
     }
 #endif
     // K3 (after K1 + K2), with stamps
-    k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, ntiles);
+    k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
     ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
     auto k3 = ccl::k_link<TY, 8, true, true, 0>;
