@@ -217,13 +217,24 @@ __device__ __forceinline__ int ld_ca(const int32_t* p) {
 __device__ __forceinline__ int find_g(int32_t* G, int a) {
     int p = ld_ca(G + a);
     CCL_LOOP_GUARD(fgh);
+#ifdef CCL_STATS
+    unsigned long long hops = 0;
+    atomicAdd(&g_stat_finds, 1ull);
+#endif
     while (p != a) {
         CCL_LOOP_TICK(fgh);
+#ifdef CCL_STATS
+        ++hops;
+#endif
         const int gp = ld_ca(G + p);
         if (gp != p) st_volatile(G + a, gp);
         a = p;
         p = gp;
     }
+#ifdef CCL_STATS
+    atomicAdd(&g_stat_hops, hops);
+    atomicMax(&g_stat_maxhops, hops);
+#endif
     return a;
 }
 // (A two-pass full path compression here -- rewriting every visited node to

@@ -188,25 +188,23 @@ int main(int argc, char** argv) {
 
 #ifdef CCL_STATS
     {
-        unsigned long long z = 0, u, st;
+        unsigned long long z = 0, u, st, nf, nh, mh;
         CK(cudaMemcpyToSymbol(ccl::g_stat_unions, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_steps, &z, 8));
         k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpyToSymbol(ccl::g_stat_finds, &z, 8));
+        CK(cudaMemcpyToSymbol(ccl::g_stat_hops, &z, 8));
+        CK(cudaMemcpyToSymbol(ccl::g_stat_maxhops, &z, 8));
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpyFromSymbol(&u, ccl::g_stat_unions, 8));
         CK(cudaMemcpyFromSymbol(&st, ccl::g_stat_steps, 8));
-        printf("K2 stats: %llu union calls, %llu walk steps (%.2f per union)\n", u, st, double(st) / u);
-        CK(cudaMemcpyToSymbol(ccl::g_stat_finds, &z, 8));
-        CK(cudaMemcpyToSymbol(ccl::g_stat_hops, &z, 8));
-        CK(cudaMemcpyToSymbol(ccl::g_stat_maxhops, &z, 8));
-        ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
-        CK(cudaDeviceSynchronize());
-        unsigned long long nf, nh, mh;
         CK(cudaMemcpyFromSymbol(&nf, ccl::g_stat_finds, 8));
         CK(cudaMemcpyFromSymbol(&nh, ccl::g_stat_hops, 8));
         CK(cudaMemcpyFromSymbol(&mh, ccl::g_stat_maxhops, 8));
-        printf("resolve stats: %llu finds, %.2f hops avg, %llu max\n", nf, double(nh) / nf, mh);
+        printf("K2 stats: %llu union calls, %llu walk steps (%.2f per union)\n", u, st, double(st) / u);
+        printf("K2 finds: %llu, %.2f hops avg, %llu max\n", nf, double(nh) / nf, mh);
     }
 #endif
     // K3 (after K1 + K2), with stamps
