@@ -400,6 +400,12 @@ __device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
 // Profiling builds only (DBG bit 2): per-tile phase timestamps.
 __device__ unsigned long long* g_k1_stamps = nullptr;
 __device__ unsigned long long* g_k3_stamps = nullptr;
+__device__ unsigned long long* g_k2_stamps = nullptr;  // per K2 task: start, end (globaltimer ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void k1_stamp(unsigned t, int k) {
     if (g_k1_stamps) g_k1_stamps[size_t(t) * 8 + k] = clock64();
 }
@@ -861,6 +867,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
     const int warp = threadIdx.x >> 5;
     // (task counts are < 2^31: <= 2 per 16 x 1024 tile; 32-bit index math)
     const unsigned task = blockIdx.x * 8u + unsigned(warp);
+    const unsigned long long t_start = (DBG & 8) ? gtimer() : 0ull;
     if (task < unsigned(n_h)) {
         if (DBG & 2) return;
         unsigned t = task;
@@ -878,6 +885,10 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         const int band0 = int(t % groups) * v_bands<TY>();
         const int b = int(t / groups);
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
+    }
+    if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < unsigned(n_h + n_v)) {
+        g_k2_stamps[2 * size_t(task)] = t_start;
+        g_k2_stamps[2 * size_t(task) + 1] = gtimer();
     }
 }
 

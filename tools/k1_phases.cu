@@ -4,6 +4,7 @@
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I include \
 //        tools/k1_phases.cu -o tools/k1_phases
 //   tools/k1_phases <raw uint8 image file> H W [conn]
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -179,6 +180,38 @@ int main(int argc, char** argv) {
     time_k2(ccl::k_boundary<TY, 8, 2>, "K2 vertical only");
     time_k2(ccl::k_boundary<TY, 8, 3>, "K2 empty (launch)");
     time_k2(ccl::k_boundary<TY, 8, 5>, "K2 horizontal, no unions");
+    {
+        // per-task K2 timeline (globaltimer): where does the kernel's time go?
+        const long long nt = n_h + n_v;
+        unsigned long long* st2;
+        CK(cudaMalloc(&st2, size_t(nt) * 16));
+        CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &st2, sizeof(st2)));
+        CK(cudaMemsetAsync(flush, 1, fb));
+        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+        ccl::k_boundary<TY, 8, 8><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
+        CK(cudaDeviceSynchronize());
+        std::vector<unsigned long long> hs(size_t(nt) * 2);
+        CK(cudaMemcpy(hs.data(), st2, hs.size() * 8, cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull, t1 = 0;
+        for (long long i = 0; i < nt; ++i) { t0 = std::min(t0, hs[2 * i]); t1 = std::max(t1, hs[2 * i + 1]); }
+        printf("K2 timeline: span %.1f us over %lld tasks\n", (t1 - t0) / 1000.0, nt);
+        for (int kind = 0; kind < 2; ++kind) {
+            std::vector<double> d, st, en;
+            for (long long i = kind ? n_h : 0; i < (kind ? nt : n_h); ++i) {
+                d.push_back((hs[2 * i + 1] - hs[2 * i]) / 1000.0);
+                st.push_back((hs[2 * i] - t0) / 1000.0);
+                en.push_back((hs[2 * i + 1] - t0) / 1000.0);
+            }
+            if (d.empty()) continue;
+            auto pct = [](std::vector<double> v, double q) { std::sort(v.begin(), v.end()); return v[size_t(q * (v.size() - 1))]; };
+            printf("  %s: dur p50 %.2f p90 %.2f p99 %.2f max %.2f | start p50 %.2f max %.2f | end p50 %.2f p99 %.2f max %.2f us\n",
+                   kind ? "vertical  " : "horizontal", pct(d, .5), pct(d, .9), pct(d, .99), pct(d, 1.0), pct(st, .5),
+                   pct(st, 1.0), pct(en, .5), pct(en, .99), pct(en, 1.0));
+        }
+        CK(cudaFree(st2));
+        unsigned long long* np = nullptr;
+        CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &np, sizeof(np)));
+    }
     {
         k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
