@@ -354,12 +354,16 @@ struct K1Smem {
 };
 
 // find / merge of §2.1.3 over tile run ids.
+#ifdef CCL_STATS
+__device__ unsigned long long g_stat_k1_unions = 0, g_stat_k1_steps = 0, g_stat_k1_hops = 0;
+#endif
 __device__ __forceinline__ int find_r(int32_t* P, int a) {
     volatile int32_t* V = P;
     int p = V[a];
     CCL_LOOP_GUARD(fr);
     while (p != a) {
         CCL_LOOP_TICK(fr);
+        CCL_STAT(g_stat_k1_hops);
         const int gp = V[p];
         if (gp != p) V[a] = gp;  // path halving: re-point at an ancestor
         a = p;
@@ -386,7 +390,9 @@ __device__ __forceinline__ int find_r_ro(const int32_t* P, int a) {
 // the smaller with atomicMin; if someone else re-linked it first, retry with
 // the value it was linked to.
 __device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
+    CCL_STAT(g_stat_k1_unions);
     while (true) {
+        CCL_STAT(g_stat_k1_steps);
         a = find_r(P, a);
         b = find_r(P, b);
         if (a == b) return;
@@ -395,6 +401,18 @@ __device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
         if (old == a) return;
         a = old;
     }
+}
+
+// K1's union call; profiling variants (DBG bit 8: skipped, bit 16: one
+// atomicMin without finds -- timing only, the labels are then wrong).
+template <int DBG>
+__device__ __forceinline__ void k1_union(int32_t* P, int a, int b) {
+    if (DBG & 8) return;
+    if (DBG & 16) {
+        atomicMin(&P[a], b);
+        return;
+    }
+    union_r(P, a, b);
 }
 
 // Profiling builds only (DBG bit 2): per-tile phase timestamps.
@@ -513,13 +531,13 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             const WordE u = sm.wd[r - 1][p >> 5];
             const int open = (u.m & 1u) && !(u.s & 1u);
             const int j = sm.rbase[r - 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r] && (rs[j] & 1023) <= q) union_r(P, k, j);
+            if (j < sm.rbase[r] && (rs[j] & 1023) <= q) k1_union<DBG>(P, k, j);
         }
         if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
             const WordE u = sm.wd[r + 1][p >> 5];
             const int open = (u.m & 1u) && !(u.s & 1u);
             const int j = sm.rbase[r + 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r + 2] && (rs[j] & 1023) <= q) union_r(P, j, k);
+            if (j < sm.rbase[r + 2] && (rs[j] & 1023) <= q) k1_union<DBG>(P, j, k);
         }
     }
     __syncthreads();

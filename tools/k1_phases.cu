@@ -121,11 +121,15 @@ int main(int argc, char** argv) {
     g.div_tx = ccl::FastDiv(g.tiles_x);
     g.div_ty = ccl::FastDiv(g.tiles_y);
     g.label_off = g.force_top = g.force_bottom = 0;
-    for (int per_sm : {2, 3}) {
+    for (int per_sm : {3, 4}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
         snprintf(nm, sizeof nm, "K1 load+convert+runs (DBG=3) x%d", per_sm);
         run_k1<TY, 8, 3>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
+        snprintf(nm, sizeof nm, "K1 +UF loop, no unions (DBG=10) x%d", per_sm);
+        run_k1<TY, 8, 10>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
+        snprintf(nm, sizeof nm, "K1 +UF one atomic each (DBG=18) x%d", per_sm);
+        run_k1<TY, 8, 18>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
         snprintf(nm, sizeof nm, "K1 +local UF (DBG=2) x%d", per_sm);
         run_k1<TY, 8, 2>(nm, img, g, bits, G, R, E, ntiles, grid, flush, fb);
         snprintf(nm, sizeof nm, "K1 full (DBG=0) x%d", per_sm);
@@ -237,6 +241,19 @@ int main(int argc, char** argv) {
         CK(cudaMemcpyFromSymbol(&nh, ccl::g_stat_hops, 8));
         CK(cudaMemcpyFromSymbol(&mh, ccl::g_stat_maxhops, 8));
         printf("K2 stats: %llu union calls, %llu walk steps (%.2f per union)\n", u, st, double(st) / u);
+        {
+            unsigned long long ku, ks, kh;
+            CK(cudaMemcpyToSymbol(ccl::g_stat_k1_unions, &z, 8));
+            CK(cudaMemcpyToSymbol(ccl::g_stat_k1_steps, &z, 8));
+            CK(cudaMemcpyToSymbol(ccl::g_stat_k1_hops, &z, 8));
+            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpyFromSymbol(&ku, ccl::g_stat_k1_unions, 8));
+            CK(cudaMemcpyFromSymbol(&ks, ccl::g_stat_k1_steps, 8));
+            CK(cudaMemcpyFromSymbol(&kh, ccl::g_stat_k1_hops, 8));
+            printf("K1 stats: %llu unions, %.2f steps per union, %.2f find hops per union\n", ku, double(ks) / ku,
+                   double(kh) / ku);
+        }
         printf("K2 finds: %llu, %.2f hops avg, %llu max\n", nf, double(nh) / nf, mh);
     }
 #endif
