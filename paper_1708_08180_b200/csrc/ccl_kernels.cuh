@@ -334,15 +334,15 @@ struct __align__(16) WordE {
 template <int TY>
 __host__ __device__ constexpr int k1_cap() { return TY * kTileW / 2 < 5632 ? TY * kTileW / 2 : 5632; }
 template <int TY>
-__host__ __device__ constexpr size_t k1x_slot_bytes() { return size_t(TY) * (kTileW / 2) * 8; }
+__host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
 template <int TY>
 __host__ __device__ constexpr int k1x_slots() { return TY > 16 ? 512 : 1024; }  // = max K1 grid
 
 template <int TY>
 struct K1Smem {
     WordE wd[TY][kWords];
-    uint16_t rs[k1_cap<TY>()];  // run k: start x | row << 10
-    uint16_t re[k1_cap<TY>()];  // run k: end x
+    uint16_t rs[k1_cap<TY>() + 8];  // run k: start x | row << 10; rs[total] = sentinel row 63
+    uint16_t re[k1_cap<TY>() + 8];  // run k: end x
     // parent over tile run ids (min-root forest).  After the flatten, a root
     // whose component touches a tile edge carries bit 31 and (1 + its
     // edge-list index) << 16; the low 16 bits are always the parent id.
@@ -490,6 +490,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             if (r >= TY) break;  // warp-uniform
             const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
             const WordE w = sm.wd[r][lane];
+            sm.wd[r][lane].pad = rb + w.pad;  // from here on: tile run id of the word's first start
             const int xb = lane << 5;
             int k = rb + w.pad;
             uint32_t bits_ = w.s;
@@ -508,6 +509,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
                 re[k++] = uint16_t(xb + bit);
             }
         }
+        if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
@@ -530,14 +532,16 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         if (r > 0) {  // first run of row r-1 touching [p, q]
             const WordE u = sm.wd[r - 1][p >> 5];
             const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = sm.rbase[r - 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r] && (rs[j] & 1023) <= q) k1_union<DBG>(P, k, j);
+            const int j = u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            const int rsj = rs[j];  // j may be the next row's first run or the sentinel
+            if ((rsj >> 10) == r - 1 && (rsj & 1023) <= q) k1_union<DBG>(P, k, j);
         }
         if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
             const WordE u = sm.wd[r + 1][p >> 5];
             const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = sm.rbase[r + 1] + u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            if (j < sm.rbase[r + 2] && (rs[j] & 1023) <= q) k1_union<DBG>(P, j, k);
+            const int j = u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
+            const int rsj = rs[j];
+            if ((rsj >> 10) == r + 1 && (rsj & 1023) <= q) k1_union<DBG>(P, j, k);
         }
     }
     __syncthreads();
@@ -685,7 +689,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         k1_runs<TY, CONN, DBG>(sm, sm.rs, sm.re, sm.P, g, t, id, v, total, G, R, E, warp, lane);
     } else {
         char* slot = static_cast<char*>(k1x) + size_t(blockIdx.x) * k1x_slot_bytes<TY>();
-        constexpr int N = TY * kTileW / 2;
+        constexpr int N = TY * kTileW / 2 + 8;
         k1_runs<TY, CONN, DBG>(sm, reinterpret_cast<uint16_t*>(slot), reinterpret_cast<uint16_t*>(slot) + N,
                                reinterpret_cast<int32_t*>(slot + 4 * N), g, t, id, v, total, G, R, E, warp, lane);
     }
