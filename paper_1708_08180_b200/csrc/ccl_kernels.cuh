@@ -529,20 +529,16 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         const int rsk = rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
         const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        if (r > 0) {  // first run of row r-1 touching [p, q]
-            const WordE u = sm.wd[r - 1][p >> 5];
-            const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            const int rsj = rs[j];  // j may be the next row's first run or the sentinel
-            if ((rsj >> 10) == r - 1 && (rsj & 1023) <= q) k1_union<DBG>(P, k, j);
-        }
-        if (r + 1 < TY) {  // first run of row r+1 touching [p, q]
-            const WordE u = sm.wd[r + 1][p >> 5];
-            const int open = (u.m & 1u) && !(u.s & 1u);
-            const int j = u.pad - open + __popc(u.e & ((1u << (p & 31)) - 1u));
-            const int rsj = rs[j];
-            if ((rsj >> 10) == r + 1 && (rsj & 1023) <= q) k1_union<DBG>(P, j, k);
-        }
+        // first runs of rows r-1 and r+1 touching [p, q] (both searches are
+        // issued before either union: the phase is bound by this chain)
+        const WordE uu = sm.wd[r > 0 ? r - 1 : 0][p >> 5];
+        const WordE ud = sm.wd[r + 1 < TY ? r + 1 : TY - 1][p >> 5];
+        const uint32_t below = (1u << (p & 31)) - 1u;
+        const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
+        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
+        const int rsu = rs[ju], rsd = rs[jd];  // may be another row's run or the sentinel
+        if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
+        if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) k1_union<DBG>(P, jd, k);
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
