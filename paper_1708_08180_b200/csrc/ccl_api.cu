@@ -52,6 +52,9 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.nwords = H * int64_t(p.g.WW);
     p.g.div_tx = ccl::FastDiv(unsigned(p.g.tiles_x));
     p.g.div_ty = ccl::FastDiv(unsigned(p.g.tiles_y));
+    p.g.div_ty1 = ccl::FastDiv(unsigned(std::max(1, p.g.tiles_y - 1)));
+    p.g.div_tx1 = ccl::FastDiv(unsigned(std::max(1, p.g.tiles_x - 1)));
+    p.g.div_vg = ccl::FastDiv(unsigned((p.g.tiles_y + 32 / tile_rows - 1) / (32 / tile_rows)));
     p.g.label_off = 0;
     p.g.force_top = 0;
     p.g.force_bottom = 0;

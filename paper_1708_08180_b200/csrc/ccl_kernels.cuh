@@ -76,6 +76,7 @@ struct Geom {
     long long npx;     // H*W  (per image)
     long long nwords;  // H*WW (per image)
     FastDiv div_tx, div_ty;  // by tiles_x, tiles_y
+    FastDiv div_ty1, div_tx1, div_vg;  // K2 task decode: tiles_y - 1, tiles_x - 1, vertical task groups
     // strip mode (row-strip sharding of one image over several GPUs):
     int label_off;     // added to every label (row0 * W_total: labels are global)
     int force_top;     // the image's first row borders another strip
@@ -726,7 +727,7 @@ __device__ __forceinline__ size_t tile_index(const Geom& g, int b, int ty, int t
 }
 
 // The horizontal boundary above tile (b, band >= 1, tx); one warp.
-constexpr int kPairsPerLane = 8;  // boundary pairs a lane contributes per round
+constexpr int kPairsPerLane = 4;  // boundary pairs a lane contributes per round
 
 template <int TY, int CONN, bool NOUNION = false>
 __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
@@ -744,12 +745,20 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     CCL_ASSERT(up_base >= 0 && up_base < RCAP);
     const uint32_t* Rup = R + t_up * RCAP + up_base;  // last row's runs
     const int wg = tx * kWords + lane;
-    const uint32_t cur = wg < g.WW ? __ldcg(bm + size_t(y0) * g.WW + wg) : 0u;
-    const uint32_t up = wg < g.WW ? __ldcg(bm + size_t(y0 - 1) * g.WW + wg) : 0u;
-    uint32_t sc, su;
-    int cc, cu;
-    row_runs(cur, lane, sc, cc);
-    row_runs(up, lane, su, cu);
+    const uint32_t* rowc = bm + size_t(y0) * g.WW;
+    const uint32_t* rowu = rowc - g.WW;
+    const uint32_t cur = wg < g.WW ? __ldcg(rowc + wg) : 0u;
+    const uint32_t up = wg < g.WW ? __ldcg(rowu + wg) : 0u;
+    // the words diagonally across the tile corners, loaded with the rows (no
+    // second round trip): upper row, word left of the tile / right of it
+    uint32_t corner = 0;
+    if (CONN == 8 && lane == 0 && tx > 0) corner = __ldcg(rowu + wg - 1);
+    if (CONN == 8 && lane == 31 && x0 + kTileW < g.W) corner = __ldcg(rowu + wg + 1);
+    uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
+    uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
+    if (lane == 0) { curL = 0; upL = 0; }
+    if (lane == 31) { curR = 0; upR = 0; }
+    const uint32_t sc = cur & ~((cur << 1) | (curL >> 31)), su = up & ~((up << 1) | (upL >> 31));
     // row-local run index of the first start in each word (prefix of popc)
     int ic = __popc(sc), iu = __popc(su);
 #pragma unroll
@@ -757,13 +766,9 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         const int a = __shfl_up_sync(kFull, ic, d), c = __shfl_up_sync(kFull, iu, d);
         if (lane >= d) { ic += a; iu += c; }
     }
-    s_w[0][lane] = Word{cur, sc, cc, ic - __popc(sc)};
-    s_w[1][lane] = Word{up, su, cu, iu - __popc(su)};
+    s_w[0][lane] = Word{cur, sc, 0, ic - __popc(sc)};
+    s_w[1][lane] = Word{up, su, 0, iu - __popc(su)};
     __syncwarp();
-    uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
-    uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
-    if (lane == 0) { curL = 0; upL = 0; }
-    if (lane == 31) { curR = 0; upR = 0; }
     const uint32_t o = cur & up, oL = curL & upL;
     uint32_t ev = o & ~((o << 1) | (oL >> 31));
     uint32_t ne = 0, nw = 0;
@@ -773,8 +778,8 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
         ne = cur & ~cur_n & ~up & up_n;
         nw = cur & ~cur_p & ~up & up_p;
-        if (lane == 0 && tx > 0 && (cur & 1u)) cnw = __ldcg(bm + size_t(y0 - 1) * g.WW + wg - 1) >> 31;
-        if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = __ldcg(bm + size_t(y0 - 1) * g.WW + wg + 1) & 1u;
+        if (lane == 0 && tx > 0 && (cur & 1u)) cnw = corner >> 31;
+        if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = corner & 1u;
     }
     // run index (within its row) of the run containing foreground pixel x:
     // (number of run starts at positions <= x) - 1
@@ -801,35 +806,53 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
             if (lane >= d) incl += u;
         }
         const int total = __shfl_sync(kFull, incl, 31);
-        int pos = incl - take;
-        for (int e = 0; e < take; ++e) {
-            int a, c;
-            if (ev) {
-                const int x = (lane << 5) + __ffs(ev) - 1;
-                ev &= ev - 1;
-                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-                c = rec_root(__ldcg(Rup + run_idx(1, x)), W, x0, y0 - TY);
-            } else if (ne) {
-                const int x = (lane << 5) + __ffs(ne) - 1;
-                ne &= ne - 1;
-                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-                c = rec_root(__ldcg(Rup + run_idx(1, x + 1)), W, x0, y0 - TY);
-            } else if (nw) {
-                const int x = (lane << 5) + __ffs(nw) - 1;
-                nw &= nw - 1;
-                a = rec_root(__ldcg(Rlo + run_idx(0, x)), W, x0, y0);
-                c = rec_root(__ldcg(Rup + run_idx(1, x - 1)), W, x0, y0 - TY);
-            } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
-                cnw = false;
-                a = __ldcg(E + t_lo * kEdgeCap + kEdgeLC);
-                c = __ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1);
-            } else {  // cne: (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
-                cne = false;
-                a = __ldcg(E + t_lo * kEdgeCap + kEdgeRC);
-                c = __ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1);
+        const int pos = incl - take;
+        // all of this lane's record loads are issued before any is used (one
+        // round trip per round instead of one per event)
+        uint32_t va[kPairsPerLane], vc[kPairsPerLane];
+        unsigned raw = 0;  // bit e: the pair is two roots already (tile-corner diagonals)
+#pragma unroll
+        for (int e = 0; e < kPairsPerLane; ++e) {
+            if (e < take) {
+                if (ev | ne | nw) {
+                    int x, xu;
+                    if (ev) {
+                        x = (lane << 5) + __ffs(ev) - 1;
+                        ev &= ev - 1;
+                        xu = x;
+                    } else if (ne) {
+                        x = (lane << 5) + __ffs(ne) - 1;
+                        ne &= ne - 1;
+                        xu = x + 1;
+                    } else {
+                        x = (lane << 5) + __ffs(nw) - 1;
+                        nw &= nw - 1;
+                        xu = x - 1;
+                    }
+                    va[e] = __ldcg(Rlo + run_idx(0, x));
+                    vc[e] = __ldcg(Rup + run_idx(1, xu));
+                } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
+                    cnw = false;
+                    va[e] = uint32_t(__ldcg(E + t_lo * kEdgeCap + kEdgeLC));
+                    vc[e] = uint32_t(__ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1));
+                    raw |= 1u << e;
+                } else {  // cne: (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
+                    cne = false;
+                    va[e] = uint32_t(__ldcg(E + t_lo * kEdgeCap + kEdgeRC));
+                    vc[e] = uint32_t(__ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1));
+                    raw |= 1u << e;
+                }
             }
-            CCL_ASSERT(a >= 0 && a < g.npx && c >= 0 && c < g.npx);
-            pairs[pos++] = make_int2(a, c);
+        }
+#pragma unroll
+        for (int e = 0; e < kPairsPerLane; ++e) {
+            if (e < take) {
+                const bool r = (raw >> e) & 1u;
+                const int a = r ? int(va[e]) : rec_root(va[e], W, x0, y0);
+                const int c = r ? int(vc[e]) : rec_root(vc[e], W, x0, y0 - TY);
+                CCL_ASSERT(a >= 0 && a < g.npx && c >= 0 && c < g.npx);
+                pairs[pos + e] = make_int2(a, c);
+            }
         }
         __syncwarp();
         for (int base = 0; base < total; base += 32) {
@@ -888,20 +911,21 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
     const unsigned long long t_start = (DBG & 8) ? gtimer() : 0ull;
     if (task < unsigned(n_h)) {
         if (DBG & 2) return;
-        unsigned t = task;
-        const int tx = int(t % unsigned(g.tiles_x));
-        t /= unsigned(g.tiles_x);
-        const int band = 1 + int(t % unsigned(g.tiles_y - 1));
-        const int b = int(t / unsigned(g.tiles_y - 1));
+        const unsigned q = g.div_tx.div(task);
+        const int tx = int(task - q * unsigned(g.tiles_x));
+        const unsigned q2 = g.div_ty1.div(q);
+        const int band = 1 + int(q - q2 * unsigned(g.tiles_y - 1));
+        const int b = int(q2);
         boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp]);
     } else if (task < unsigned(n_h + n_v)) {
         if (DBG & 1) return;
-        unsigned t = task - unsigned(n_h);
-        const int bx = 1 + int(t % unsigned(g.tiles_x - 1));
-        t /= unsigned(g.tiles_x - 1);
+        const unsigned t = task - unsigned(n_h);
+        const unsigned q = g.div_tx1.div(t);
+        const int bx = 1 + int(t - q * unsigned(g.tiles_x - 1));
+        const unsigned q2 = g.div_vg.div(q);
         const unsigned groups = unsigned(g.tiles_y + v_bands<TY>() - 1) / v_bands<TY>();
-        const int band0 = int(t % groups) * v_bands<TY>();
-        const int b = int(t / groups);
+        const int band0 = int(q - q2 * groups) * v_bands<TY>();
+        const int b = int(q2);
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
     }
     if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < unsigned(n_h + n_v)) {

@@ -120,6 +120,9 @@ int main(int argc, char** argv) {
     const unsigned ntiles = g.tiles_x * g.tiles_y;
     g.div_tx = ccl::FastDiv(g.tiles_x);
     g.div_ty = ccl::FastDiv(g.tiles_y);
+    g.div_ty1 = ccl::FastDiv(std::max(1, g.tiles_y - 1));
+    g.div_tx1 = ccl::FastDiv(std::max(1, g.tiles_x - 1));
+    g.div_vg = ccl::FastDiv((g.tiles_y + 32 / TY - 1) / (32 / TY));
     g.label_off = g.force_top = g.force_bottom = 0;
     for (int per_sm : {3, 4}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
