@@ -329,11 +329,14 @@ struct __align__(16) WordE {
 
 // Run lists of a tile live in shared memory up to k1_cap runs (natural
 // images: a few hundred; i.i.d. noise at density 1/2: ~4096), which keeps the
-// block at ~55 KB -- 4 blocks (32 warps) per SM.  A tile with more runs
-// (period-2 stripes, checkerboards: up to TY*512) keeps them in the block's
-// slot of a global scratch area instead (same code, L2-resident).
+// block at 45 KB -- with one prefetch register set (44 registers) 5 blocks
+// (40 warps) per SM; measured: 4 blocks 46.8 us, 5 blocks 43.6 us on C3
+// texture (a cap of 4096 also allowed 5 blocks but sent half the noise tiles
+// to the scratch path).  A tile with more runs (period-2 stripes,
+// checkerboards: up to TY*512) keeps them in the block's slot of a global
+// scratch area instead (same code, L2-resident).
 template <int TY>
-__host__ __device__ constexpr int k1_cap() { return TY * kTileW / 2 < 5632 ? TY * kTileW / 2 : 5632; }
+__host__ __device__ constexpr int k1_cap() { return TY * kTileW / 2 < 4576 ? TY * kTileW / 2 : 4576; }
 template <int TY>
 __host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
 template <int TY>
@@ -621,8 +624,8 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
 
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
-                                        const ImgRegs<TY>& cur, uint32_t* bits, int32_t* G,
-                                        uint32_t* R, int32_t* E, void* k1x, int warp, int lane) {
+                                        ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
+                                        int32_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
@@ -666,6 +669,9 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
         k1_row_init<TY>(sm, r, lane, m);
     }
+    // the pixels are in the masks now: the same registers receive the block's
+    // next tile, in flight during the rest of this one
+    if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, cur);
     if (tid < TY) sm.lc[tid] = -1;
     else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
     else if (tid == 2 * TY) sm.ecount = 0;
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads1, 4) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+__global__ void __launch_bounds__(kThreads1, 5) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              int32_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
@@ -954,19 +960,13 @@ __global__ void __launch_bounds__(kThreads1, 4) k_local_merge(const uint8_t* __r
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
     constexpr bool PF = VEC && k1_prefetches<TY>();
-    // two register sets used alternately (no copies): a holds tile t while b
-    // receives tile t + gridDim.x, then the roles swap
-    ImgRegs<TY> a, b;
+    // one register set: loaded with tile t before the loop, then refilled with
+    // the block's next tile as soon as the current one is in the masks
+    ImgRegs<TY> a;
     if (PF) k1_prefetch<TY>(img, g, t, warp, lane, a);
-    while (true) {
-        if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, b);
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, bits, G, R, E, k1x, warp, lane);
+    while (t < ntiles) {
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, k1x, warp, lane);
         t += gridDim.x;
-        if (t >= ntiles) break;
-        if (PF && t + gridDim.x < ntiles) k1_prefetch<TY>(img, g, t + gridDim.x, warp, lane, a);
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, b, bits, G, R, E, k1x, warp, lane);
-        t += gridDim.x;
-        if (t >= ntiles) break;
     }
 }
 
