@@ -124,7 +124,7 @@ int main(int argc, char** argv) {
     g.div_tx1 = ccl::FastDiv(std::max(1, g.tiles_x - 1));
     g.div_vg = ccl::FastDiv((g.tiles_y + 32 / TY - 1) / (32 / TY));
     g.label_off = g.force_top = g.force_bottom = 0;
-    for (int per_sm : {3, 4}) {
+    for (int per_sm : {4, 5}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
         snprintf(nm, sizeof nm, "K1 load+convert+runs (DBG=3) x%d", per_sm);
@@ -140,12 +140,12 @@ int main(int argc, char** argv) {
     }
     run_k1<TY, 8, 0>("K1 full, one block per tile", img, g, bits, G, R, E, ntiles, ntiles, flush, fb);
 
-    // per-phase clock64 stamps (DBG bit 2), persistent grid x3
+    // per-phase clock64 stamps (DBG bit 2), persistent grid x5
     unsigned long long* st;
     CK(cudaMalloc(&st, size_t(ntiles) * 8 * 8));
     CK(cudaMemset(st, 0, size_t(ntiles) * 8 * 8));
     CK(cudaMemcpyToSymbol(ccl::g_k1_stamps, &st, sizeof(st)));
-    run_k1<TY, 8, 4>("K1 full + stamps x3", img, g, bits, G, R, E, ntiles, std::min<int>(ntiles, sms * 3), flush, fb);
+    run_k1<TY, 8, 4>("K1 full + stamps x5", img, g, bits, G, R, E, ntiles, std::min<int>(ntiles, sms * 5), flush, fb);
     std::vector<unsigned long long> hs(size_t(ntiles) * 8);
     CK(cudaMemcpy(hs.data(), st, hs.size() * 8, cudaMemcpyDeviceToHost));
     const char* names[6] = {"convert+row init", "run lists", "union", "flatten", "edges+G", "run records"};
@@ -160,7 +160,7 @@ int main(int argc, char** argv) {
 
     // K2 variants (each preceded by K1, which resets the G entries K2 touches)
     auto k1 = ccl::k_local_merge<TY, 8, true, 0>;
-    const int grid1 = std::min<int>(ntiles, sms * 3);
+    const int grid1 = std::min<int>(ntiles, sms * 5);
     const size_t sm1 = sizeof(ccl::K1Smem<TY>);
     const long long n_h = (long long)(g.tiles_y - 1) * g.tiles_x, n_v = (long long)((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) * (g.tiles_x - 1);
     const long long bh = (n_h + n_v + 7) / 8, bv = 0;
