@@ -13,8 +13,8 @@ HEADER = os.path.join(ROOT, "include", "ccl.h")
 
 @pytest.fixture(scope="module")
 def ccl():
-    from paper_1708_08180_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._load_build_module().build()
     import paper_1708_08180_b200 as m
     return m
 
