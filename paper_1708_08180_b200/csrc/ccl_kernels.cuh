@@ -156,6 +156,43 @@ __device__ __forceinline__ void st_stream_i4(int32_t* p, int a, int b, int c, in
                  : "memory");
 }
 
+// K1's outputs (bit mask, run records, edge blocks, parent sectors) are stored
+// with an L2 evict_last hint: the boundary analysis and K3 read them back
+// right after K1, and without the hint most of them were already evicted
+// again by K1's own 64 MiB image stream (ncu, cache control off: K2 / resolve
+// L2 read hit rates 25 % / 21 %, K1 writing its 12.5 MB back to DRAM).
+#ifndef CCL_K1_KEEP
+#define CCL_K1_KEEP 1
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void l2_discard(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void st_keep(T* p, T v) {
+    static_assert(sizeof(T) == 4, "32-bit stores");
+#if CCL_K1_KEEP
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(*reinterpret_cast<uint32_t*>(&v)),
+                 "l"(l2_keep_policy())
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void st_keep_v4(int4* p, int4 v) {
+#if CCL_K1_KEEP
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(l2_keep_policy())
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
+
 __device__ __forceinline__ int ld_volatile(const int32_t* p) {
     return *reinterpret_cast<const volatile int32_t*>(p);
 }
@@ -580,17 +617,17 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             if (!(atomicOr(&P[root], int(0x80000000u)) & int(0x80000000u))) {
                 const int idx = atomicAdd(&sm.ecount, 1);
                 P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
-                Et[idx] = gr;
+                st_keep(Et + idx, gr);
                 if ((g.npx & 7) == 0) {
                     // whole sector, identity: harmless for the 7 neighbours
                     // (every root entry is still its own index during K1, all
                     // other entries are never read); images are sector-aligned
                     const int base = gr & ~7;
                     int4* sec = reinterpret_cast<int4*>(Gb + base);
-                    sec[0] = make_int4(base, base + 1, base + 2, base + 3);
-                    sec[1] = make_int4(base + 4, base + 5, base + 6, base + 7);
+                    st_keep_v4(sec, make_int4(base, base + 1, base + 2, base + 3));
+                    st_keep_v4(sec + 1, make_int4(base + 4, base + 5, base + 6, base + 7));
                 } else {
-                    Gb[gr] = gr;
+                    st_keep(Gb + gr, gr);
                 }
             }
             if (lc) sm.lc[r] = gr;
@@ -606,17 +643,17 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
     // edge block header + column roots, and the per-run records for K3 / K2
     if (tid == 0) {
-        Eh[0] = sm.ecount;
-        Eh[1] = sm.rbase[last_row];  // first run of the last valid row
+        st_keep(Eh, sm.ecount);
+        st_keep(Eh + 1, sm.rbase[last_row]);  // first run of the last valid row
     }
-    if (tid < TY) Eh[kEdgeLC + tid] = sm.lc[tid];
-    else if (tid < 2 * TY) Eh[kEdgeRC + tid - TY] = sm.rc[tid - TY];
+    if (tid < TY) st_keep(Eh + kEdgeLC + tid, sm.lc[tid]);
+    else if (tid < 2 * TY) st_keep(Eh + kEdgeRC + tid - TY, sm.rc[tid - TY]);
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int root = P[k] & 0xFFFF;
         const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
-        Rt[k] = uint32_t(rs[root]) | (uint32_t(tag) << 16);
+        st_keep(Rt + k, uint32_t(rs[root]) | (uint32_t(tag) << 16));
     }
     __syncthreads();  // smem is reused by the next tile
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
@@ -666,7 +703,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
             }
         }
         const int wg = id.tx * kWords + lane;
-        if (y < g.H && wg < g.WW) bm[size_t(y) * g.WW + wg] = m;
+        if (y < g.H && wg < g.WW) st_keep(bm + size_t(y) * g.WW + wg, m);
         k1_row_init<TY>(sm, r, lane, m);
     }
     // the pixels are in the masks now: the same registers receive the block's
@@ -1115,7 +1152,8 @@ __device__ __forceinline__ int selp_nz(uint32_t x, int a, int b) {
 __device__ __forceinline__ int swz(int w, int g) { return (w << 3) + (g ^ (w & 7)); }
 
 template <int TY, int CONN, bool VEC, bool TMA, int DBG = 0>
-__device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, unsigned t, const LinkRegs<TY>& cur,
+__device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const uint32_t* bits, unsigned t,
+                                        const LinkRegs<TY>& cur,
                                         const uint32_t* R, const int32_t* F, int32_t* out,
                                         const CUtensorMap* tmap, int warp, int lane) {
     const TileId id = decode_tile<TY>(g, t);
@@ -1253,6 +1291,23 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, unsigne
         r0 = r1;
         __syncthreads();  // the table (and, after the last window, all smem) is reused
     }
+#ifndef CCL_K3_DISCARD
+#define CCL_K3_DISCARD 1
+#endif
+#if CCL_K1_KEEP && CCL_K3_DISCARD
+    // K1's mask rows and run records of this tile have had their last reader:
+    // drop their (evict_last, dirty) L2 lines without a DRAM write-back.  Only
+    // whole 128-byte lines owned by this tile (mask rows when W % 1024 == 0).
+    {
+        const int total = __shfl_sync(kFull, v, TY - 1);
+        for (int i = tid; i < (total + 31) / 32; i += kThreads) l2_discard(Rt + 32 * i);
+        if ((W & 1023) == 0 && lane < TY / kWarps) {
+            const int y = y0 + warp + lane * kWarps;
+            if (y < g.H)
+                l2_discard(bits + size_t(id.b) * size_t(g.nwords) + size_t(y) * g.WW + id.tx * kWords);
+        }
+    }
+#endif
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 3);
 }
 
@@ -1272,11 +1327,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_link(Geom g, const uint32_t* __
     k3_prefetch<TY>(bits, R, F, g, t, warp, lane, a);
     while (true) {
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, b);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, t, a, R, F, out, &tmap, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, a, R, F, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, a);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, t, b, R, F, out, &tmap, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, b, R, F, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
     }
