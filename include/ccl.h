@@ -109,7 +109,10 @@ ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64
  *                          tile-edge entries of the parent array (workspace).
  *   ccl_stage_boundary     K2: unions every foreground edge that crosses a tile
  *                          boundary into the parent array (workspace only).
- *   ccl_stage_link         K3: writes labels_out for every pixel.          */
+ *   ccl_stage_link         K3: resolves the tile-edge roots to their final
+ *                          labels (the last step of the boundary analysis,
+ *                          done by K3's helper warps) and writes labels_out
+ *                          for every pixel.                                */
 ccl_status_t ccl_stage_local_merge(const uint8_t* images, int64_t B, int64_t H, int64_t W,
                                    int connectivity, void* workspace, size_t workspace_bytes,
                                    int tile_rows, void* stream);

@@ -101,11 +101,18 @@ cudaError_t setup_attrs() {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem_bytes_k1<TY>()));
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem_bytes<TY>()));
-        if (e != cudaSuccess) return e;
-        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem_bytes<TY>()));
+        const int sm3 = int(smem_bytes<TY>());
+        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+            return e;
+        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+            return e;
+        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+            return e;
+        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
     }();
     return once;
 }
@@ -188,7 +195,7 @@ int persistent_blocks(int which) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads1,
                                                       smem_bytes_k1<TY>());
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC, true>, ccl::kThreads,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC, true, true>, ccl::kK3Threads,
                                                       smem_bytes<TY>());
     cached[w][dev] = std::max(1, sms) * std::max(1, b);
     return cached[w][dev];
@@ -229,10 +236,14 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
                            (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v);
             if (e != cudaSuccess) return e;
         }
-        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-        e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, G, (const int32_t*)E, F,
-                       unsigned(ntiles));
-        if (e != cudaSuccess) return e;
+        // the resolve step (edge roots -> final labels) runs in K3's helper
+        // warps; the strip stages need the labels in F before K3, so there it
+        // is its own launch
+        if (stages & kStripEdges) {
+            const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
+            e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, G, (const int32_t*)E, F, unsigned(ntiles));
+            if (e != cudaSuccess) return e;
+        }
     }
     if (stages & kStripEdges) {
         // edge-root marks (Gs = out as scratch), boundary-row labels, slot reps
@@ -256,17 +267,17 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     }
     if (stages & kK3) {
         // labels leave through TMA bulk-tensor stores when rows are 32-px
-        // multiples (all bench configs); else 128-bit st.global.cs
+        // multiples (all bench configs); else 128-bit st.global.cs.  The
+        // helper warp resolves the edge roots (RES), or in strip mode takes
+        // the patched labels from F.
         CUtensorMap map;
         std::memset(&map, 0, sizeof(map));
-        if (VEC && g.W % 32 == 0 && encode_label_map(&map, out, g))
-            e = launch_pdl(ccl::k_link<TY, CONN, VEC, true>, grid3, ccl::kThreads, smem, s, g,
-                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)F, out, unsigned(ntiles),
-                           map);
-        else
-            e = launch_pdl(ccl::k_link<TY, CONN, VEC, false>, grid3, ccl::kThreads, smem, s, g,
-                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)F, out, unsigned(ntiles),
-                           map);
+        const bool tma = VEC && g.W % 32 == 0 && encode_label_map(&map, out, g);
+        const bool res = !(stages & kStripFinalize);
+        auto k3 = tma ? (res ? ccl::k_link<TY, CONN, VEC, true, true> : ccl::k_link<TY, CONN, VEC, true, false>)
+                      : (res ? ccl::k_link<TY, CONN, VEC, false, true> : ccl::k_link<TY, CONN, VEC, false, false>);
+        e = launch_pdl(k3, grid3, ccl::kK3Threads, smem, s, g, (const uint32_t*)bits, (const uint32_t*)runs,
+                       (const int32_t*)E, G, (const int32_t*)F, out, unsigned(ntiles), map);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

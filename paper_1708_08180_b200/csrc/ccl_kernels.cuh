@@ -141,6 +141,8 @@ __device__ __forceinline__ uint32_t nz16(uint4 v) {
 // slower (K3's blocks then hold shared memory the resolve / boundary blocks
 // need; 173 us with triggers at kernel entry, 148 with one in resolve).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// K3's barrier over its 256 compute threads (named barrier 1; the helper warp never joins)
+__device__ __forceinline__ void k3_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
 // Read-once image loads (no L1 allocation).  An L2 evict-first cache policy
 // on these loads measured slower for K1 and did not help K2 (profiles r01).
@@ -1085,7 +1087,9 @@ struct __align__(1024) LinkSmem {
     LWord wd[TY][kWords];
     int32_t lab[kLabCap];            // final label of tile run k (current row window)
     uint4 rc[kRunCache / 4];         // first run records of the tile (prefetched)
-    int32_t fc[kEdgeCache];          // first resolved edge labels (prefetched)
+    int32_t fl[2][kEdgeCap - kEdgeList];  // final labels of the edge roots of tiles j, j+1 (helper warp)
+    int32_t produced;                // tiles whose fl slot the helper warp has filled
+    int32_t consumed;                // tiles whose fl slot the compute warps are done with
     int32_t rcnt[TY];
     int32_t rbase[TY + 1];
 };
@@ -1094,11 +1098,10 @@ template <int TY>
 struct LinkRegs {
     uint32_t m[TY / kWarps];
     uint4 runs;  // warps 0, 2: run records 4*i .. 4*i+3 (i = lane, 32 + lane)
-    int fin;     // warp 1: resolved label F[lane]
 };
 
 template <int TY>
-__device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t* R, const int32_t* F,
+__device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t* R,
                                             const Geom& g, unsigned t, int warp, int lane,
                                             LinkRegs<TY>& pf) {
     const TileId id = decode_tile<TY>(g, t);
@@ -1112,7 +1115,6 @@ __device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t
     if (warp == 0 || warp == 2)
         pf.runs = __ldg(reinterpret_cast<const uint4*>(R + size_t(t) * runs_per_tile_cap<TY>()) + lane +
                         (warp == 2 ? 32 : 0));
-    if (warp == 1) pf.fin = __ldg(F + size_t(t) * kEdgeCap + lane);
 }
 
 // TMA bulk-tensor store of one 1024-px label row from shared memory: the
@@ -1152,19 +1154,20 @@ __device__ __forceinline__ int selp_nz(uint32_t x, int a, int b) {
 __device__ __forceinline__ int swz(int w, int g) { return (w << 3) + (g ^ (w & 7)); }
 
 template <int TY, int CONN, bool VEC, bool TMA, int DBG = 0>
-__device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const uint32_t* bits, unsigned t,
-                                        const LinkRegs<TY>& cur,
-                                        const uint32_t* R, const int32_t* F, int32_t* out,
+__device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const uint32_t* bits, unsigned t, int j,
+                                        const LinkRegs<TY>& cur, const uint32_t* R, int32_t* out,
                                         const CUtensorMap* tmap, int warp, int lane) {
     const TileId id = decode_tile<TY>(g, t);
     int32_t* ob = out + size_t(id.b) * size_t(g.npx);
     const uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
-    const int32_t* Ft = F + size_t(t) * kEdgeCap;
+    const int32_t* Fl = sm.fl[j & 1];
     const int tid = threadIdx.x;
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 0);
 
     if (warp == 0 || warp == 2) sm.rc[lane + (warp == 2 ? 32 : 0)] = cur.runs;
-    if (warp == 1) sm.fc[lane] = cur.fin;
+    if (tid == 0) {  // the helper warp has this tile's edge labels in slot j & 1
+        while (ld_volatile(&sm.produced) <= j) __nanosleep(32);
+    }
     // 1. run starts and run numbering of every row
 #pragma unroll
     for (int i = 0; i < TY / kWarps; ++i) {
@@ -1183,7 +1186,7 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
         sm.wd[r][lane] = LWord{m, incl - n};
         if (lane == 31) sm.rcnt[r] = incl;
     }
-    __syncthreads();
+    k3_sync();
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 1);
     // run base of every row (lane r of every warp: v = first run id of row r+1)
     int v = lane < TY ? sm.rcnt[lane] : 0;
@@ -1211,10 +1214,10 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
             const int e = int(rec >> 16);  // 1 + edge-list index, or 0
             const int rr = int(rec & 0x7FFFu);
             int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
-            if (e) lab = e <= kEdgeCache ? sm.fc[e - 1] : __ldg(Ft + e - 1);
+            if (e) lab = Fl[e - 1];
             sm.lab[k - base] = lab;
         }
-        __syncthreads();
+        k3_sync();
         if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 2);
 
         // 3. expand and stream the window's rows
@@ -1289,7 +1292,7 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
             }
         }
         r0 = r1;
-        __syncthreads();  // the table (and, after the last window, all smem) is reused
+        k3_sync();  // the table (and, after the last window, all smem) is reused
     }
 #ifndef CCL_K3_DISCARD
 #define CCL_K3_DISCARD 1
@@ -1308,30 +1311,97 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
         }
     }
 #endif
+    if (tid == 0) *reinterpret_cast<volatile int32_t*>(&sm.consumed) = j + 1;  // slot j & 1 is free again
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 3);
 }
 
-template <int TY, int CONN, bool VEC, bool TMA = false, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, 3) k_link(Geom g, const uint32_t* __restrict__ bits,
-                                                      const uint32_t* __restrict__ R,
-                                                      const int32_t* __restrict__ F,
-                                                      int32_t* __restrict__ out, unsigned ntiles,
-                                                      const __grid_constant__ CUtensorMap tmap) {
+// K3's helper warp (warp 8): the final labels of each of the block's tiles'
+// edge roots, one tile ahead of the compute warps, into the shared slot
+// j & 1.  RES: resolved here from the parent forest (the boundary analysis'
+// resolve step, moved off its own launch into K3's bandwidth-bound shadow):
+// concurrent pointer jumping -- every edge root is owned by exactly one
+// thread, which keeps re-pointing its own entry at the grandparent it reads,
+// so chains shared by many roots collapse in ~log d rounds; entries only ever
+// move to ancestors.  !RES (strip mode): copy the labels the strip stages left
+// in F.
+template <int TY, bool RES>
+__device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const int32_t* E, int32_t* G,
+                                          const int32_t* F, unsigned ntiles) {
+    const int lane = threadIdx.x & 31;
+    const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
+    int j = 0;
+    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        if (lane == 0) {  // slot j & 1 was last used by tile j - 2
+            while (ld_volatile(&sm.consumed) < j - 1) __nanosleep(64);
+        }
+        __syncwarp();
+        const int32_t* Et = E + size_t(t) * kEdgeCap;
+        const int n = __ldcg(Et);
+        int32_t* slot = sm.fl[j & 1];
+        if (RES) {
+            int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
+            for (int i = lane; i < n; i += 32) {
+                const int x = __ldcg(Et + kEdgeList + i);
+                int p = __ldcg(Gb + x);
+                CCL_LOOP_GUARD(pj);
+                if (p != x) {
+                    while (true) {
+                        CCL_LOOP_TICK(pj);
+                        const int gp = __ldcg(Gb + p);
+                        if (gp == p) break;
+                        CCL_ASSERT(gp < p);
+                        __stcg(Gb + x, gp);
+                        p = gp;
+                    }
+                }
+                slot[i] = p + 1 + g.label_off;
+            }
+        } else {
+            for (int i = lane; i < n; i += 32) slot[i] = __ldcg(F + size_t(t) * kEdgeCap + i);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            *reinterpret_cast<volatile int32_t*>(&sm.produced) = j + 1;
+        }
+    }
+}
+
+constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
+
+template <int TY, int CONN, bool VEC, bool TMA = false, bool RES = true, int DBG = 0>
+__global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* __restrict__ bits,
+                                                        const uint32_t* __restrict__ R,
+                                                        const int32_t* __restrict__ E,
+                                                        int32_t* __restrict__ G,
+                                                        const int32_t* __restrict__ F,
+                                                        int32_t* __restrict__ out, unsigned ntiles,
+                                                        const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     LinkSmem<TY>& sm = *reinterpret_cast<LinkSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        sm.produced = 0;
+        sm.consumed = 0;
+    }
+    __syncthreads();
     pdl_wait();
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
+    if (warp == kWarps) {
+        k3_helper<TY, RES>(sm, g, E, G, F, ntiles);
+        return;
+    }
     LinkRegs<TY> a, b;
-    k3_prefetch<TY>(bits, R, F, g, t, warp, lane, a);
+    k3_prefetch<TY>(bits, R, g, t, warp, lane, a);
+    int j = 0;
     while (true) {
-        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, b);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, a, R, F, out, &tmap, warp, lane);
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, j++, a, R, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
-        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, F, g, t + gridDim.x, warp, lane, a);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, b, R, F, out, &tmap, warp, lane);
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, a);
+        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, j++, b, R, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;
     }

@@ -264,8 +264,8 @@ int main(int argc, char** argv) {
     k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
     ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
-    auto k3 = ccl::k_link<TY, 8, true, true, 0>;
-    auto k3s = ccl::k_link<TY, 8, true, true, 4>;
+    auto k3 = ccl::k_link<TY, 8, true, true, false, 0>;
+    auto k3s = ccl::k_link<TY, 8, true, true, false, 4>;
     const size_t sm3 = sizeof(ccl::LinkSmem<TY>);
     CUtensorMap tmap;
     {
@@ -284,19 +284,19 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(k3s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     for (int per_sm : {3, 4, 5}) {
         const int grid3 = std::min<int>(ntiles, sms * per_sm);
-        float us = timeit([&] { k3<<<grid3, ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
+        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
         printf("K3 x%d                              %8.1f us\n", per_sm, us);
     }
     {
-        auto k3z = ccl::k_link<TY, 8, true, true, 1>;
+        auto k3z = ccl::k_link<TY, 8, true, true, false, 1>;
         CK(cudaFuncSetAttribute(k3z, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
-        float us = timeit([&] { k3z<<<std::min<int>(ntiles, sms * 3), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
+        float us = timeit([&] { k3z<<<std::min<int>(ntiles, sms * 3), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
         printf("K3 x3, no expansion (stale rowbuf)  %8.1f us\n", us);
     }
     unsigned long long* st3;
     CK(cudaMalloc(&st3, size_t(ntiles) * 8 * 8));
     CK(cudaMemcpyToSymbol(ccl::g_k3_stamps, &st3, sizeof(st3)));
-    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kThreads, sm3>>>(g, bits, R, F, out, ntiles, tmap); }, flush, fb);
+    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
     printf("K3 + stamps x4                     %8.1f us\n", us3);
     CK(cudaMemcpy(hs.data(), st3, hs.size() * 8, cudaMemcpyDeviceToHost));
     const char* n3[3] = {"row runs", "label table", "expand+write"};
