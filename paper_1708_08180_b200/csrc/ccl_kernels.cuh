@@ -232,9 +232,14 @@ __device__ __forceinline__ void st_volatile(int32_t* p, int v) {
 #ifdef CCL_STATS
 __device__ unsigned long long g_stat_unions = 0, g_stat_steps = 0, g_stat_finds = 0, g_stat_hops = 0,
                               g_stat_maxhops = 0;
+// per K2 task (profiling harness): [0] union walk steps, [1] find hops, [2] link
+// retries, [3] rounds (task = blockIdx.x * 8 + warp)
+__device__ unsigned* g_k2_taskstat = nullptr;
 #define CCL_STAT(v) atomicAdd(&(v), 1ull)
+#define CCL_TASKSTAT(k, n) (g_k2_taskstat ? (void)atomicAdd(g_k2_taskstat + 4 * (blockIdx.x * 8u + (threadIdx.x >> 5)) + (k), (n)) : (void)0)
 #else
 #define CCL_STAT(v) ((void)0)
+#define CCL_TASKSTAT(k, n) ((void)0)
 #endif
 
 // Global min-union (reading R11).  The finds use L1-cacheable loads: many
@@ -274,6 +279,7 @@ __device__ __forceinline__ int find_g(int32_t* G, int a) {
 #ifdef CCL_STATS
     atomicAdd(&g_stat_hops, hops);
     atomicMax(&g_stat_maxhops, hops);
+    CCL_TASKSTAT(1, unsigned(hops));
 #endif
     return a;
 }
@@ -288,12 +294,14 @@ __device__ __forceinline__ void union_g(int32_t* G, int a, int b) {
     while (true) {
         CCL_LOOP_TICK(ug);
         CCL_STAT(g_stat_steps);
+        CCL_TASKSTAT(0, 1u);
         a = find_g(G, a);
         b = find_g(G, b);
         if (a == b) return;
         if (a < b) { int t = a; a = b; b = t; }
         const int old = atomicMin(G + a, b);
         if (old == a) return;
+        CCL_TASKSTAT(2, 1u);
         a = old;
     }
 }
@@ -375,11 +383,14 @@ struct __align__(16) WordE {
 // checkerboards: up to TY*512) keeps them in the block's slot of a global
 // scratch area instead (same code, L2-resident).
 template <int TY>
-__host__ __device__ constexpr int k1_cap() { return TY * kTileW / 2 < 4576 ? TY * kTileW / 2 : 4576; }
+__host__ __device__ constexpr int k1_cap() {
+    // TY = 32: 16 KB of row words; 3456 runs keep the block at 44 KB (5 per SM)
+    return TY * kTileW / 2 < (TY > 16 ? 3456 : 4576) ? TY * kTileW / 2 : (TY > 16 ? 3456 : 4576);
+}
 template <int TY>
 __host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
 template <int TY>
-__host__ __device__ constexpr int k1x_slots() { return TY > 16 ? 512 : 1024; }  // = max K1 grid
+__host__ __device__ constexpr int k1x_slots() { return TY > 16 ? 768 : 1024; }  // = max K1 grid (148 SMs x 5)
 
 template <int TY>
 struct K1Smem {
@@ -711,6 +722,17 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     // the pixels are in the masks now: the same registers receive the block's
     // next tile, in flight during the rest of this one
     if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, cur);
+    // tall tiles (no register room for a second tile): the next tile's rows
+    // are pulled into L2 with bulk prefetches instead, one per row
+    if (VEC && !k1_prefetches<TY>() && tnext < ntiles && warp == kWarps1 - 1 && lane < TY) {
+        const TileId nx = decode_tile<TY>(g, tnext);
+        const int y = nx.y0 + lane;
+        if (y < g.H) {
+            const uint8_t* row = img + size_t(nx.b) * size_t(g.npx) + size_t(y) * size_t(g.W) + nx.x0;
+            const unsigned bytes = unsigned(min(kTileW, g.W - nx.x0));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"(bytes) : "memory");
+        }
+    }
     if (tid < TY) sm.lc[tid] = -1;
     else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
     else if (tid == 2 * TY) sm.ecount = 0;
@@ -842,6 +864,7 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     // spread over all 32 lanes (a lane with many events no longer serialises
     // the warp's union latency).
     while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
+        if (lane == 0) CCL_TASKSTAT(3, 1u);
         const int have = __popc(ev) + __popc(ne) + __popc(nw) + int(cnw) + int(cne);
         const int take = min(have, kPairsPerLane);
         int incl = take;

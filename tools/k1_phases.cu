@@ -215,6 +215,35 @@ int main(int argc, char** argv) {
                    kind ? "vertical  " : "horizontal", pct(d, .5), pct(d, .9), pct(d, .99), pct(d, 1.0), pct(st, .5),
                    pct(st, 1.0), pct(en, .5), pct(en, .99), pct(en, 1.0));
         }
+#ifdef CCL_STATS
+        {   // the slowest tasks: what do they do?
+            unsigned* ts;
+            CK(cudaMalloc(&ts, size_t(nt) * 16));
+            CK(cudaMemset(ts, 0, size_t(nt) * 16));
+            CK(cudaMemcpyToSymbol(ccl::g_k2_taskstat, &ts, sizeof(ts)));
+            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
+            CK(cudaDeviceSynchronize());
+            std::vector<unsigned> hts(size_t(nt) * 4);
+            CK(cudaMemcpy(hts.data(), ts, hts.size() * 4, cudaMemcpyDeviceToHost));
+            std::vector<long long> idx(nt);
+            for (long long i = 0; i < nt; ++i) idx[i] = i;
+            std::sort(idx.begin(), idx.end(), [&](long long x, long long y) {
+                return hs[2 * x + 1] - hs[2 * x] > hs[2 * y + 1] - hs[2 * y];
+            });
+            double sst = 0, sho = 0, sre = 0, sro = 0;
+            for (long long i = 0; i < nt; ++i) { sst += hts[4*i]; sho += hts[4*i+1]; sre += hts[4*i+2]; sro += hts[4*i+3]; }
+            printf("K2 per task mean: steps %.1f hops %.1f retries %.2f rounds %.2f\n", sst / nt, sho / nt, sre / nt, sro / nt);
+            for (int k = 0; k < 12 && k < nt; ++k) {
+                const long long i = idx[k];
+                printf("  slow task %lld (%s): %.2f us  steps %u hops %u retries %u rounds %u\n", i, i < n_h ? "h" : "v",
+                       (hs[2 * i + 1] - hs[2 * i]) / 1000.0, hts[4*i], hts[4*i+1], hts[4*i+2], hts[4*i+3]);
+            }
+            unsigned* np2 = nullptr;
+            CK(cudaMemcpyToSymbol(ccl::g_k2_taskstat, &np2, sizeof(np2)));
+            CK(cudaFree(ts));
+        }
+#endif
         CK(cudaFree(st2));
         unsigned long long* np = nullptr;
         CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &np, sizeof(np)));
