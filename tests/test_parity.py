@@ -154,6 +154,16 @@ def test_c3_8192(ccl, kind, conn):
     assert_same(gpu_label(ccl, img, conn), oracle.label_bfs(img, conn), f"C3 {kind}")
 
 
+@pytest.mark.parametrize("conn", CONNS)
+def test_c3_tile_rows_32(ccl, conn):
+    # 32-row tiles: 2048 tiles over a persistent grid of ~740 blocks, so every
+    # block takes several tiles (the L2 bulk prefetch of its next tile), and a
+    # noise band that overflows the 3456-run shared-memory cap (scratch path)
+    img = synth.texture(8192, 8192, seed=3001, density=0.5)
+    img[4096:4160] = synth.noise(64, 8192, 0.5, seed=7)
+    assert_same(gpu_label(ccl, img, conn, tile_rows=32), oracle.label_bfs(img, conn), "C3 texture, tile_rows=32")
+
+
 def test_c4_frames_sampled(ccl):
     """C4 at full size (1024 x 1080x1920, one batched call, as bench times it):
     16 sampled frames compared element by element with the oracle."""
