@@ -97,6 +97,16 @@ template <int TY, int CONN, bool VEC>
 cudaError_t setup_attrs() {
     // opt in to > 48 KB dynamic shared memory once per instantiation
     static cudaError_t once = [] {
+#ifndef CCL_K2_CARVEOUT
+#define CCL_K2_CARVEOUT 40
+#endif
+        // K2's finds are served from L1 (ld.global.ca): a 40 % shared-memory
+        // carveout (100 KB: 5-6 resident 16 KB blocks) leaves the rest of the
+        // 256 KB to L1.  Measured, C3 K2 µs: default (no hint) 26-29 and
+        // varying between runs, 100 % 25, 40 % 24.5, 0 % 49 (blocks no
+        // longer all resident); noise 80 / 65 / 56 / 149.
+        cudaFuncSetAttribute(ccl::k_boundary<TY, CONN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             CCL_K2_CARVEOUT);
         cudaError_t e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem_bytes_k1<TY>()));
