@@ -1346,42 +1346,55 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
 // thread, which keeps re-pointing its own entry at the grandparent it reads,
 // so chains shared by many roots collapse in ~log d rounds; entries only ever
 // move to ancestors.  !RES (strip mode): copy the labels the strip stages left
-// in F.
+// in F.  k3_resolve_tile does one tile's roots i = first, first + stride, ...
+constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
+
+template <bool RES>
+__device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, int32_t* G,
+                                                const int32_t* F, unsigned t, int first, int stride) {
+    const int32_t* Et = E + size_t(t) * kEdgeCap;
+    const int n = __ldcg(Et);
+    if (RES) {
+        const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
+        int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
+        for (int i = first; i < n; i += stride) {
+            const int x = __ldcg(Et + kEdgeList + i);
+            int p = __ldcg(Gb + x);
+            CCL_LOOP_GUARD(pj);
+            if (p != x) {
+                while (true) {
+                    CCL_LOOP_TICK(pj);
+                    const int gp = __ldcg(Gb + p);
+                    if (gp == p) break;
+                    CCL_ASSERT(gp < p);
+                    __stcg(Gb + x, gp);
+                    p = gp;
+                }
+            }
+            slot[i] = p + 1 + g.label_off;
+        }
+    } else {
+        for (int i = first; i < n; i += stride) slot[i] = __ldcg(F + size_t(t) * kEdgeCap + i);
+    }
+}
+
+#ifndef CCL_K3_COOP
+#define CCL_K3_COOP 1
+#endif
+
+// The helper warp's loop over the block's tiles j0, j0+1, ... (t = blockIdx.x
+// + j * gridDim.x).
 template <int TY, bool RES>
 __device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const int32_t* E, int32_t* G,
-                                          const int32_t* F, unsigned ntiles) {
+                                          const int32_t* F, unsigned ntiles, int j0) {
     const int lane = threadIdx.x & 31;
-    const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
-    int j = 0;
-    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+    int j = j0;
+    for (unsigned t = blockIdx.x + unsigned(j0) * gridDim.x; t < ntiles; t += gridDim.x, ++j) {
         if (lane == 0) {  // slot j & 1 was last used by tile j - 2
             while (ld_volatile(&sm.consumed) < j - 1) __nanosleep(64);
         }
         __syncwarp();
-        const int32_t* Et = E + size_t(t) * kEdgeCap;
-        const int n = __ldcg(Et);
-        int32_t* slot = sm.fl[j & 1];
-        if (RES) {
-            int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
-            for (int i = lane; i < n; i += 32) {
-                const int x = __ldcg(Et + kEdgeList + i);
-                int p = __ldcg(Gb + x);
-                CCL_LOOP_GUARD(pj);
-                if (p != x) {
-                    while (true) {
-                        CCL_LOOP_TICK(pj);
-                        const int gp = __ldcg(Gb + p);
-                        if (gp == p) break;
-                        CCL_ASSERT(gp < p);
-                        __stcg(Gb + x, gp);
-                        p = gp;
-                    }
-                }
-                slot[i] = p + 1 + g.label_off;
-            }
-        } else {
-            for (int i = lane; i < n; i += 32) slot[i] = __ldcg(F + size_t(t) * kEdgeCap + i);
-        }
+        k3_resolve_tile<RES>(sm.fl[j & 1], g, E, G, F, t, lane, 32);
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
@@ -1390,7 +1403,6 @@ __device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const
     }
 }
 
-constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
 
 template <int TY, int CONN, bool VEC, bool TMA = false, bool RES = true, int DBG = 0>
 __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* __restrict__ bits,
@@ -1411,8 +1423,18 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
     pdl_wait();
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
+    // The block's first tile: all 9 warps resolve its edge roots together
+    // (one chain latency instead of n / 32 of them on the helper alone -- the
+    // compute warps would otherwise wait for it); the helper takes the rest.
+    int j0 = 0;
+    if (CCL_K3_COOP) {
+        k3_resolve_tile<RES>(sm.fl[0], g, E, G, F, t, threadIdx.x, kK3Threads);
+        __syncthreads();
+        if (threadIdx.x == 0) sm.produced = 1;
+        j0 = 1;
+    }
     if (warp == kWarps) {
-        k3_helper<TY, RES>(sm, g, E, G, F, ntiles);
+        k3_helper<TY, RES>(sm, g, E, G, F, ntiles, j0);
         return;
     }
     LinkRegs<TY> a, b;
