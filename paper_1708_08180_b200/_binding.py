@@ -4,7 +4,7 @@ supplies device memory (caching allocator) and the current CUDA stream.
 
 There is deliberately no fallback: if libccl.so is missing or cannot be
 loaded, importing this module raises (build it with
-``python -m paper_1708_08180_b200._build`` or ``__graft_entry__.build()``).
+``python paper_1708_08180_b200/_build.py`` or ``__graft_entry__.build()``).
 """
 from __future__ import annotations
 
@@ -15,7 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libccl.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1708_08180_b200._build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1708_08180_b200/_build.py` "
                       "(there is no CPU fallback)")
 _lib = ctypes.CDLL(LIB_PATH)
 
