@@ -123,6 +123,28 @@ ccl_status_t ccl_stage_link(int64_t B, int64_t H, int64_t W, int connectivity,
                             int32_t* labels_out, void* workspace, size_t workspace_bytes,
                             int tile_rows, void* stream);
 
+/* The paper's comparison methods (Table 2; SURVEY.md 8(f)
+ * NEXT-1), on B200, for measuring the paper's relative claims -- not product
+ * paths.  Same problem, conventions and canonical output as ccl_label:
+ *   CCL_METHOD_OPTIMIZED  this library's three-kernel path (= ccl_label_batched_async)
+ *   CCL_METHOD_UF         conventional parallel UF [oliveira2010study]
+ *                         (PAPER.md:37, 68-70): per-pixel local UF in shared
+ *                         memory over {32,16,1} blocks, global merge of every
+ *                         tile-boundary pixel, per-pixel link
+ *   CCL_METHOD_LINE_UF    line-based UF [yonehara2015line]:
+ *                         {512,1,1} row segments, global UF over all cells
+ *   CCL_METHOD_LE         label equivalence: multi-pass;
+ *                         reads a convergence flag back every iteration, so
+ *                         this call SYNCHRONISES the stream and returns when done
+ * Workspace: >= ccl_method_workspace_bytes(...) device bytes (0 = invalid
+ * geometry or method).  Unknown method -> CCL_ERR_CONFIG; B or H > 65535 ->
+ * CCL_ERR_DIMS (grid limits of the pixel-level launches). */
+enum { CCL_METHOD_OPTIMIZED = 0, CCL_METHOD_UF = 1, CCL_METHOD_LINE_UF = 2, CCL_METHOD_LE = 3 };
+size_t ccl_method_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity, int method);
+ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                    int connectivity, int method, int32_t* labels_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of K2 boundary work items for the given geometry and tile height:
  * horizontal tile-edge segments (one warp each) and vertical tile-edge pixels
  * (one thread each).  Host-only bookkeeping (cf. Eq. (1)-(2), PAPER.md:326-334,

@@ -12,6 +12,9 @@ CUDA behind the C ABI in include/ccl.h); this package only marshals arguments.
 from ._binding import (  # noqa: F401
     CCLError,
     HostSession,
+    METHODS,
+    MethodWorkspace,
+    label_method,
     StripLabeler,
     label_strips_emulated,
     strip_bounds,
@@ -27,5 +30,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
            "stages", "stage_fns", "status_string", "raw"]

@@ -39,7 +39,12 @@ SIGNATURES = {
     "ccl_strip_workspace_bytes": (_sz, [_i64, _i64, _int, _int]),
     "ccl_strip_local": (_int, [_vp, _i64, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _sz, _vp]),
     "ccl_strip_finalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
+    "ccl_method_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int]),
+    "ccl_label_method_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp]),
 }
+
+# the paper's comparison methods (include/ccl.h CCL_METHOD_*)
+METHODS = {"optimized": 0, "uf": 1, "line_uf": 2, "le": 3}
 
 for _name, (_res, _args) in SIGNATURES.items():
     _fn = getattr(_lib, _name)
@@ -150,6 +155,44 @@ def label(image, connectivity: int = 8, *, out=None, workspace: Workspace | None
     _check(_lib.ccl_label_batched_cfg_async(
         ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
         workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(stream)), "ccl_label_batched_cfg_async")
+    return out
+
+
+class MethodWorkspace:
+    """Device workspace for label_method (one of METHODS)."""
+
+    def __init__(self, B: int, H: int, W: int, connectivity: int, method: str, device=None):
+        torch = _torch()
+        n = int(_lib.ccl_method_workspace_bytes(B, H, W, connectivity, METHODS[method]))
+        if n == 0:
+            raise ValueError("invalid geometry or method")
+        self.nbytes = n
+        self.buf = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+
+    def ptr(self):
+        return ctypes.c_void_p(self.buf.data_ptr())
+
+
+def label_method(image, connectivity: int = 8, method: str = "uf", *, out=None,
+                 workspace: MethodWorkspace | None = None, stream=None):
+    """Label with one of the paper's comparison methods (conventional UF,
+    line-based UF, label equivalence; or "optimized" = this library's path)
+    through ccl_label_method_async.  Same canonical output as label()."""
+    torch = _torch()
+    _check_image(image)
+    B, H, W = _shape3(image)
+    if method not in METHODS:
+        raise ValueError(f"method must be one of {sorted(METHODS)}")
+    if out is None:
+        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+    if B == 0:
+        return out
+    if workspace is None:
+        workspace = MethodWorkspace(B, H, W, connectivity, method, device=image.device)
+    _check(_lib.ccl_label_method_async(
+        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), METHODS[method],
+        ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, _stream_ptr(stream)),
+        "ccl_label_method_async")
     return out
 
 

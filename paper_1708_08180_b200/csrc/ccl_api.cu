@@ -3,6 +3,7 @@
 #include "../../include/ccl.h"
 #include "ccl_kernels.cuh"
 #include "ccl_strip.cuh"
+#include "ccl_baselines.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -325,6 +326,50 @@ ccl_status_t run(const Plan& p, int conn, int stages, const uint8_t* img, int32_
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
 }
 
+template <int CONN>
+cudaError_t run_method(int method, const uint8_t* img, int B, int H, int W, int32_t* out, void* ws, cudaStream_t s) {
+    namespace cb = ccl::base;
+    const long long npx = (long long)H * W, n = npx * B;
+    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, 148LL * 16));
+    int32_t* G = static_cast<int32_t*>(ws);
+    if (method == CCL_METHOD_UF) {
+        const dim3 grid((W + cb::kBX - 1) / cb::kBX, (H + cb::kBY - 1) / cb::kBY, B);
+        cb::k_uf_local<CONN><<<grid, dim3(cb::kBX, cb::kBY), 0, s>>>(img, H, W, npx, G);
+        const int nrows = (H - 1) / cb::kBY, ncols = 2 * ((W + cb::kBX - 1) / cb::kBX);
+        const long long per = (long long)nrows * W + (long long)ncols * H;
+        if (per > 0) cb::k_uf_global<CONN><<<dim3(unsigned((per + 255) / 256), B), 256, 0, s>>>(img, H, W, npx, G, nrows, ncols, per);
+        cb::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, out, n, npx);
+        return cudaGetLastError();
+    }
+    if (method == CCL_METHOD_LINE_UF) {
+        const dim3 grid((W + cb::kLine - 1) / cb::kLine, H, B);
+        cb::k_line_local<<<grid, cb::kLine, 0, s>>>(img, H, W, npx, G);
+        cb::k_line_global<CONN><<<grid, cb::kLine, 0, s>>>(img, H, W, npx, G);
+        cb::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, out, n, npx);
+        return cudaGetLastError();
+    }
+    // LE: iterate scan / analysis / relabel until a scan changes nothing
+    int32_t* L = G;
+    int32_t* R = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + align_up(size_t(n) * sizeof(int32_t)));
+    int* changed = reinterpret_cast<int*>(reinterpret_cast<char*>(R) + align_up(size_t(n) * sizeof(int32_t)));
+    cb::k_le_init<<<flat_blocks, 256, 0, s>>>(img, L, R, n, npx);
+    const dim3 grid((W + cb::kBX - 1) / cb::kBX, (H + cb::kBY - 1) / cb::kBY, B);
+    cudaError_t e;
+    for (int it = 0;; ++it) {
+        if ((e = cudaMemsetAsync(changed, 0, sizeof(int), s)) != cudaSuccess) return e;
+        cb::k_le_scan<CONN><<<grid, dim3(cb::kBX, cb::kBY), 0, s>>>(L, R, H, W, npx, changed);
+        int h = 0;
+        if ((e = cudaMemcpyAsync(&h, changed, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+        if (!h) break;
+        cb::k_le_analysis<<<flat_blocks, 256, 0, s>>>(L, R, n, npx);
+        cb::k_le_relabel<<<flat_blocks, 256, 0, s>>>(L, R, n, npx);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    cb::k_le_out<<<flat_blocks, 256, 0, s>>>(L, out, n);
+    return cudaGetLastError();
+}
+
 ccl_status_t validate_buffers(const Plan& p, const uint8_t* img, const int32_t* out, void* ws,
                               size_t ws_bytes, int stages) {
     const size_t n = size_t(p.g.B) * size_t(p.g.npx);
@@ -413,6 +458,39 @@ ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H
                                      size_t workspace_bytes, void* stream) {
     return ccl_label_batched_cfg_async(images, B, H, W, connectivity, labels_out, workspace,
                                        workspace_bytes, 0, stream);
+}
+
+// ----------------------------------------- the paper's comparison methods
+// (kernels in ccl_baselines.cuh)
+size_t ccl_method_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity, int method) {
+    if (method == CCL_METHOD_OPTIMIZED) return ccl_workspace_bytes(B, H, W, connectivity);
+    if (check_geometry(B, H, W, connectivity) != CCL_OK) return 0;
+    const size_t n = size_t(B) * size_t(H) * size_t(W);
+    if (method == CCL_METHOD_UF || method == CCL_METHOD_LINE_UF) return align_up(n * sizeof(int32_t));
+    if (method == CCL_METHOD_LE) return 2 * align_up(n * sizeof(int32_t)) + kAlign;
+    return 0;
+}
+
+ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H, int64_t W, int connectivity,
+                                    int method, int32_t* labels_out, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+    if (method == CCL_METHOD_OPTIMIZED)
+        return ccl_label_batched_async(images, B, H, W, connectivity, labels_out, workspace, workspace_bytes, stream);
+    ccl_status_t st = check_geometry(B, H, W, connectivity);
+    if (st != CCL_OK) return st;
+    if (method != CCL_METHOD_UF && method != CCL_METHOD_LINE_UF && method != CCL_METHOD_LE) return CCL_ERR_CONFIG;
+    if (B == 0) return CCL_OK;
+    if (B > 65535 || H > 65535) return CCL_ERR_DIMS;  // grid.z = B, (line UF) grid.y = H
+    if (!images || !labels_out || !workspace) return CCL_ERR_NULL;
+    if (workspace_bytes < ccl_method_workspace_bytes(B, H, W, connectivity, method)) return CCL_ERR_WORKSPACE;
+    const size_t n = size_t(B) * size_t(H) * size_t(W);
+    if (overlaps(images, n, labels_out, n * 4) || overlaps(images, n, workspace, workspace_bytes) ||
+        overlaps(labels_out, n * 4, workspace, workspace_bytes))
+        return CCL_ERR_ALIAS;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const cudaError_t e = connectivity == 4 ? run_method<4>(method, images, int(B), int(H), int(W), labels_out, workspace, s)
+                                            : run_method<8>(method, images, int(B), int(H), int(W), labels_out, workspace, s);
+    return e == cudaSuccess ? CCL_OK : cuda_fail(e);
 }
 
 static ccl_status_t stage(const uint8_t* images, int64_t B, int64_t H, int64_t W, int conn,
