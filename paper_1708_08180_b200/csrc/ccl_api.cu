@@ -18,6 +18,7 @@ namespace {
 thread_local int g_last_cuda_error = 0;
 
 constexpr int kDefaultTileRows = 16;
+constexpr int64_t kSmallTiles = 148 * 4;  // below this many 16-row tiles: 8-row tiles
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
@@ -39,7 +40,18 @@ ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
 ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows, Plan& p) {
     ccl_status_t st = check_geometry(B, H, W, conn);
     if (st != CCL_OK) return st;
-    if (tile_rows == 0) tile_rows = kDefaultTileRows;
+    if (tile_rows == 0) {
+        // Default tile height: 16 rows; 8 when 16-row tiles would not give
+        // the persistent K1 grid (148 SMs x 4-5 blocks) a tile per block --
+        // small images are latency-bound per tile (C1 512^2 noise 74 -> 56 us,
+        // C2 2048^2 noise 130 -> 102 us).  CCL_TILE_AUTO=0 disables the rule.
+        static const bool autoty = [] {
+            const char* v = std::getenv("CCL_TILE_AUTO");
+            return !(v && v[0] == '0');
+        }();
+        const int64_t tiles16 = B * ((W + ccl::kTileW - 1) / ccl::kTileW) * ((H + 15) / 16);
+        tile_rows = (autoty && tiles16 < kSmallTiles) ? 8 : kDefaultTileRows;
+    }
     if (tile_rows != 8 && tile_rows != 16 && tile_rows != 32) return CCL_ERR_CONFIG;
     if (B > INT32_MAX) return CCL_ERR_DIMS;
     p.ty = tile_rows;
