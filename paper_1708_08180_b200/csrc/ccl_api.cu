@@ -255,8 +255,13 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
                               (g.tiles_x - 1);
         if (n_h + n_v > 0) {
-            e = launch_pdl(ccl::k_boundary<TY, CONN>, unsigned((n_h + n_v + 7) / 8), 256, 0, s, g,
-                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v);
+            // few boundaries (small images): split each horizontal one over
+            // 2 or 4 warps so the launch still fills the GPU (one task per
+            // warp, ~5900 warps resident in one wave)
+            int sub_log2 = 0;
+            while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= 148LL * 40) ++sub_log2;
+            e = launch_pdl(ccl::k_boundary<TY, CONN>, unsigned(((n_h << sub_log2) + n_v + 7) / 8), 256, 0, s, g,
+                           (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v, sub_log2);
             if (e != cudaSuccess) return e;
         }
         // the resolve step (edge roots -> final labels) runs in K3's helper

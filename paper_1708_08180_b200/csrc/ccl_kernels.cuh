@@ -799,7 +799,7 @@ constexpr int kPairsPerLane = 4;  // boundary pairs a lane contributes per round
 template <int TY, int CONN, bool NOUNION = false>
 __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
                                            const int32_t* E, int32_t* G, int b, int band, int tx,
-                                           Word (*s_w)[kWords], int2* pairs) {
+                                           Word (*s_w)[kWords], int2* pairs, int sub = 0, int sub_log2 = 0) {
     const int lane = threadIdx.x & 31;
     constexpr int RCAP = runs_per_tile_cap<TY>();
     const int x0 = tx * kTileW, y0 = band * TY;
@@ -847,6 +847,10 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         nw = cur & ~cur_p & ~up & up_p;
         if (lane == 0 && tx > 0 && (cur & 1u)) cnw = corner >> 31;
         if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = corner & 1u;
+    }
+    if ((lane >> (5 - sub_log2)) != sub) {  // another warp's share of this boundary
+        ev = ne = nw = 0;
+        cnw = cne = false;
     }
     // run index (within its row) of the run containing foreground pixel x:
     // (number of run starts at positions <= x) - 1
@@ -969,7 +973,8 @@ template <int TY, int CONN, int DBG = 0>
 __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
                                                   const uint32_t* __restrict__ R,
                                                   const int32_t* __restrict__ E,
-                                                  int32_t* __restrict__ G, long long n_h, long long n_v) {
+                                                  int32_t* __restrict__ G, long long n_h, long long n_v,
+                                                  int sub_log2 = 0) {
     __shared__ Word s_w[8][2][kWords];
     __shared__ int2 s_pairs[8][32 * kPairsPerLane];
     pdl_wait();
@@ -977,17 +982,20 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
     // (task counts are < 2^31: <= 2 per 16 x 1024 tile; 32-bit index math)
     const unsigned task = blockIdx.x * 8u + unsigned(warp);
     const unsigned long long t_start = (DBG & 8) ? gtimer() : 0ull;
-    if (task < unsigned(n_h)) {
+    const unsigned nh_sub = unsigned(n_h) << sub_log2;  // horizontal boundaries, split in 2^sub_log2 warps each
+    if (task < nh_sub) {
         if (DBG & 2) return;
-        const unsigned q = g.div_tx.div(task);
-        const int tx = int(task - q * unsigned(g.tiles_x));
+        const unsigned th = task >> sub_log2;
+        const unsigned q = g.div_tx.div(th);
+        const int tx = int(th - q * unsigned(g.tiles_x));
         const unsigned q2 = g.div_ty1.div(q);
         const int band = 1 + int(q - q2 * unsigned(g.tiles_y - 1));
         const int b = int(q2);
-        boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp]);
-    } else if (task < unsigned(n_h + n_v)) {
+        boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp],
+                                             int(task & ((1u << sub_log2) - 1u)), sub_log2);
+    } else if (task < nh_sub + unsigned(n_v)) {
         if (DBG & 1) return;
-        const unsigned t = task - unsigned(n_h);
+        const unsigned t = task - nh_sub;
         const unsigned q = g.div_tx1.div(t);
         const int bx = 1 + int(t - q * unsigned(g.tiles_x - 1));
         const unsigned q2 = g.div_vg.div(q);
@@ -996,7 +1004,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         const int b = int(q2);
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
     }
-    if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < unsigned(n_h + n_v)) {
+    if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < nh_sub + unsigned(n_v)) {
         g_k2_stamps[2 * size_t(task)] = t_start;
         g_k2_stamps[2 * size_t(task) + 1] = gtimer();
     }
