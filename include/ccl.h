@@ -145,6 +145,32 @@ ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H,
                                     int connectivity, int method, int32_t* labels_out,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Per-component statistics of a label map produced by ccl_label* (SURVEY.md
+ * 8(f) NEXT-3; "the size and location of each dot").  For image
+ * b the components are listed in increasing label order (= raster order of
+ * their minimum pixel), so record k of image b is component k+1 of the
+ * compacted numbering 1..K_b (SPEC.md:336 renumbering):
+ *   label   its label in labels (1 + minimum raster index)
+ *   area    number of pixels
+ *   x_min, y_min, x_max, y_max   inclusive bounding box
+ *   sum_x, sum_y   coordinate sums (centroid = sum / area)
+ * labels: device int32 [B][H][W], canonical (as ccl_label writes them -- any
+ * other content gives meaningless but memory-safe output).  stats: device,
+ * B * max_components records (image b at b * max_components).  counts:
+ * device int32[B], K_b; when K_b > max_components only the first
+ * max_components records are written.  Workspace >= ccl_stats_workspace_bytes.
+ * Asynchronous on `stream`.  Errors as for ccl_label (max_components < 1 ->
+ * CCL_ERR_DIMS; B > 65535 -> CCL_ERR_DIMS). */
+typedef struct {
+    int32_t label, area, x_min, y_min, x_max, y_max;
+    int64_t sum_x, sum_y;
+} ccl_component_t;
+size_t ccl_stats_workspace_bytes(int64_t B, int64_t H, int64_t W);
+ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t H, int64_t W,
+                                       int64_t max_components, ccl_component_t* stats,
+                                       int32_t* counts, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+
 /* Number of K2 boundary work items for the given geometry and tile height:
  * horizontal tile-edge segments (one warp each) and vertical tile-edge pixels
  * (one thread each).  Host-only bookkeeping (cf. Eq. (1)-(2), PAPER.md:326-334,

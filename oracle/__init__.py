@@ -13,6 +13,10 @@ Contents
                         relation, for tiny images (<= ~64 px).
 * ``canonicalize``   -- SPEC.md:441-449: relabel any labeling so each class
                         carries 1 + its minimum raster index (0 stays 0).
+* ``component_stats`` -- per-component area, bounding box and coordinate sums
+                        of a canonical label map, components in increasing
+                        label order ("size
+                        and location of each dot").
 
 Definition followed: L[p] = 0 if img[p] == 0, else
 1 + min raster index of p's 4- or 8-connected foreground component
@@ -170,3 +174,36 @@ def canonicalize(labels) -> np.ndarray:
         np.minimum.at(first, inv, pos)
         out[fgm] = (first[inv] + 1).astype(np.int32)
     return out.reshape(lab.shape)
+
+
+def component_stats(labels) -> dict:
+    """Per-component statistics of a canonical label map [H,W] (NEXT-3).
+
+    Definition (PAPER.md:27 "the size and location of each dot"; SPEC.md:336
+    renumbering 1..K in label order): for every distinct nonzero label l in
+    increasing order, with P_l = {(x, y) : labels[y, x] == l}:
+    area = |P_l|, x_min/x_max/y_min/y_max = min/max of the coordinates,
+    sum_x / sum_y = sums of the coordinates.  Library primitives only
+    (np.unique, ufunc.at)."""
+    L = np.asarray(labels)
+    H, W = L.shape
+    ys, xs = np.nonzero(L)
+    lab = L[ys, xs].astype(np.int64)
+    uniq, inv, area = np.unique(lab, return_inverse=True, return_counts=True)
+    K = len(uniq)
+    xs = xs.astype(np.int64)
+    ys = ys.astype(np.int64)
+    x_min = np.full(K, np.iinfo(np.int64).max)
+    y_min = np.full(K, np.iinfo(np.int64).max)
+    x_max = np.full(K, -1)
+    y_max = np.full(K, -1)
+    np.minimum.at(x_min, inv, xs)
+    np.minimum.at(y_min, inv, ys)
+    np.maximum.at(x_max, inv, xs)
+    np.maximum.at(y_max, inv, ys)
+    sum_x = np.zeros(K, np.int64)
+    sum_y = np.zeros(K, np.int64)
+    np.add.at(sum_x, inv, xs)
+    np.add.at(sum_y, inv, ys)
+    return {"label": uniq, "area": area.astype(np.int64), "x_min": x_min, "y_min": y_min, "x_max": x_max,
+            "y_max": y_max, "sum_x": sum_x, "sum_y": sum_y}

@@ -15,6 +15,8 @@ from ._binding import (  # noqa: F401
     METHODS,
     MethodWorkspace,
     label_method,
+    component_stats,
+    STATS_FIELDS,
     StripLabeler,
     label_strips_emulated,
     strip_bounds,
@@ -30,5 +32,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
            "stages", "stage_fns", "status_string", "raw"]

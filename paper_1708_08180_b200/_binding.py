@@ -40,6 +40,8 @@ SIGNATURES = {
     "ccl_strip_local": (_int, [_vp, _i64, _i64, _i64, _i64, _int, _int, _vp, _vp, _vp, _sz, _vp]),
     "ccl_strip_finalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
     "ccl_method_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int]),
+    "ccl_stats_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "ccl_component_stats_async": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ccl_label_method_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp]),
 }
 
@@ -194,6 +196,39 @@ def label_method(image, connectivity: int = 8, method: str = "uf", *, out=None,
         ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, _stream_ptr(stream)),
         "ccl_label_method_async")
     return out
+
+
+STATS_FIELDS = ("label", "area", "x_min", "y_min", "x_max", "y_max", "sum_x", "sum_y")
+
+
+def component_stats(labels, max_components: int | None = None, stream=None):
+    """Per-component statistics of a label map from label() (NEXT-3,
+    ccl_component_stats_async): returns (counts [B] int32, dict field ->
+    tensor [B, max_components]) with the components of each image in
+    increasing label order (record k = component k+1 of the 1..K numbering).
+    Records beyond counts[b] (or beyond max_components) are not written."""
+    torch = _torch()
+    if not isinstance(labels, torch.Tensor) or not labels.is_cuda or labels.dtype != torch.int32:
+        raise TypeError("labels must be a CUDA int32 tensor")
+    if not labels.is_contiguous():
+        raise ValueError("labels must be contiguous")
+    B, H, W = _shape3(labels)
+    if max_components is None:
+        max_components = (H * W + 1) // 2 + 1  # 4-conn checkerboard bound
+    rec = torch.empty((max(B, 1), max_components, 40), dtype=torch.uint8, device=labels.device)
+    counts = torch.zeros(max(B, 1), dtype=torch.int32, device=labels.device)
+    ws_n = int(_lib.ccl_stats_workspace_bytes(B, H, W))
+    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=labels.device)
+    _check(_lib.ccl_component_stats_async(
+        ctypes.c_void_p(labels.data_ptr()), B, H, W, int(max_components), ctypes.c_void_p(rec.data_ptr()),
+        ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws_n, _stream_ptr(stream)),
+        "ccl_component_stats_async")
+    i32 = rec.view(torch.int32)  # [B, max, 10]
+    i64 = rec.view(torch.int64)  # [B, max, 5]
+    out = {f: i32[..., k] for k, f in enumerate(STATS_FIELDS[:6])}
+    out["sum_x"] = i64[..., 3]
+    out["sum_y"] = i64[..., 4]
+    return counts[:B], {k: v[:B] for k, v in out.items()}
 
 
 def stages(image, connectivity: int, out, workspace: Workspace, tile_rows: int = 0, stream=None):

@@ -4,6 +4,7 @@
 #include "ccl_kernels.cuh"
 #include "ccl_strip.cuh"
 #include "ccl_baselines.cuh"
+#include "ccl_stats.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -507,6 +508,45 @@ ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const cudaError_t e = connectivity == 4 ? run_method<4>(method, images, int(B), int(H), int(W), labels_out, workspace, s)
                                             : run_method<8>(method, images, int(B), int(H), int(W), labels_out, workspace, s);
+    return e == cudaSuccess ? CCL_OK : cuda_fail(e);
+}
+
+// ------------------------------------------- per-component statistics
+size_t ccl_stats_workspace_bytes(int64_t B, int64_t H, int64_t W) {
+    if (check_geometry(B, H, W, 8) != CCL_OK) return 0;
+    const size_t npx = size_t(H) * size_t(W);
+    const size_t nchunks = (npx + ccl::stats::kChunk - 1) / ccl::stats::kChunk;
+    return align_up(size_t(B) * npx * sizeof(int32_t)) + align_up(size_t(B) * nchunks * sizeof(int32_t));
+}
+
+ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t H, int64_t W,
+                                       int64_t max_components, ccl_component_t* stats, int32_t* counts,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+    ccl_status_t st = check_geometry(B, H, W, 8);
+    if (st != CCL_OK) return st;
+    if (max_components < 1 || B > 65535) return CCL_ERR_DIMS;
+    if (B == 0) return CCL_OK;
+    if (!labels || !stats || !counts || !workspace) return CCL_ERR_NULL;
+    if (workspace_bytes < ccl_stats_workspace_bytes(B, H, W)) return CCL_ERR_WORKSPACE;
+    const long long npx = (long long)H * W;
+    const size_t nl = size_t(B) * size_t(npx) * 4, ns = size_t(B) * size_t(max_components) * sizeof(ccl_component_t);
+    if (overlaps(labels, nl, stats, ns) || overlaps(labels, nl, workspace, workspace_bytes) ||
+        overlaps(stats, ns, workspace, workspace_bytes) || overlaps(counts, size_t(B) * 4, stats, ns) ||
+        overlaps(counts, size_t(B) * 4, workspace, workspace_bytes) || overlaps(counts, size_t(B) * 4, labels, nl))
+        return CCL_ERR_ALIAS;
+    namespace cs = ccl::stats;
+    const int nchunks = int((npx + cs::kChunk - 1) / cs::kChunk);
+    int32_t* M = static_cast<int32_t*>(workspace);
+    int32_t* cnt = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) + align_up(size_t(B) * size_t(npx) * 4));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const dim3 gc(nchunks, unsigned(B));
+    cs::k_stats_count<<<gc, cs::kT, 0, s>>>(labels, npx, nchunks, cnt);
+    cs::k_stats_scan<<<unsigned(B), 1024, 0, s>>>(cnt, nchunks, counts);
+    cs::k_stats_rank<<<gc, cs::kT, 0, s>>>(labels, npx, int(W), nchunks, cnt, M, stats, max_components);
+    const unsigned ablocks = unsigned(std::max<long long>(1, std::min<long long>((npx + 16 * cs::kT - 1) / (16 * cs::kT),
+                                                                                   std::max<long long>(1, 148LL * 8 / B))));
+    cs::k_stats_accum<<<dim3(ablocks, unsigned(B)), cs::kT, 0, s>>>(labels, npx, int(W), M, stats, max_components);
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
 }
 
