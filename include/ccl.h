@@ -145,6 +145,20 @@ ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H,
                                     int connectivity, int method, int32_t* labels_out,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Equal-value mode: the paper's kernels compare raw
+ * pixel values (dBuff[tid] == dBuff[tid-1], PAPER.md:104, 110, 123, 127, 294,
+ * 299), so they label every region of equal value, background included, and
+ * accept grey-level input; the SPEC CPU program adopts that.
+ * Here: every pixel p gets the 0-BASED minimum raster index of its component
+ * of equal-valued, 4- or 8-connected pixels -- no
+ * background value, no +1.  Computed with the conventional-UF kernels
+ * (ccl_label_method_async's CCL_METHOD_UF) under an equality predicate.
+ * Workspace >= ccl_method_workspace_bytes(B, H, W, connectivity,
+ * CCL_METHOD_UF).  Errors as ccl_label_method_async. */
+ccl_status_t ccl_label_equal_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                   int connectivity, int32_t* labels_out, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 /* Per-component statistics of a label map produced by ccl_label* (SURVEY.md
  * 8(f) NEXT-3; "the size and location of each dot").  For image
  * b the components are listed in increasing label order (= raster order of

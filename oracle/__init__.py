@@ -13,6 +13,9 @@ Contents
                         relation, for tiny images (<= ~64 px).
 * ``canonicalize``   -- SPEC.md:441-449: relabel any labeling so each class
                         carries 1 + its minimum raster index (0 stays 0).
+* ``label_equal``    -- equal-value mode (NEXT-2): C flood fill with "same
+                        value" adjacency, every pixel labeled with its
+                        component's 0-based minimum raster index.
 * ``component_stats`` -- per-component area, bounding box and coordinate sums
                         of a canonical label map, components in increasing
                         label order ("size
@@ -63,7 +66,7 @@ def _load():
         if _lib is None:
             lib = ctypes.CDLL(build())
             sig = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]
-            for name in ("oracle_bfs", "oracle_twopass"):
+            for name in ("oracle_bfs", "oracle_twopass", "oracle_bfs_equal"):
                 fn = getattr(lib, name)
                 fn.argtypes = sig
                 fn.restype = ctypes.c_int
@@ -95,6 +98,22 @@ def _call(name: str, img, connectivity: int) -> np.ndarray:
 def label_bfs(img, connectivity: int = 8) -> np.ndarray:
     """O1: canonical labels by raster-seeded flood fill."""
     return _call("oracle_bfs", img, connectivity)
+
+
+def label_equal(img, connectivity: int = 8) -> np.ndarray:
+    """Equal-value mode (NEXT-2): every pixel labeled with the 0-based minimum
+    raster index of its component of equal-valued pixels (the paper's raw
+    value tests).  uint8 input,
+    values compared as they are."""
+    a = np.ascontiguousarray(np.asarray(img))
+    if a.dtype != np.uint8 or a.ndim != 2:
+        raise ValueError("expected a 2D uint8 image")
+    H, W = a.shape
+    out = np.empty((H, W), dtype=np.int32)
+    rc = _load().oracle_bfs_equal(a.ctypes.data, H, W, int(connectivity), out.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_bfs_equal: {ERRORS.get(rc, rc)}")
+    return out
 
 
 def label_twopass(img, connectivity: int = 8) -> np.ndarray:

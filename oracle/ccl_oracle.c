@@ -85,6 +85,47 @@ int oracle_bfs(const uint8_t* img, int64_t H, int64_t W, int conn, int32_t* out)
     return O_OK;
 }
 
+/* Equal-value mode (the paper's raw-value tests
+ * dBuff[tid] == dBuff[tid-1], and the
+ * SPEC CPU program's semantics): every pixel, background
+ * included, belongs to the component of equal-valued neighbours; its label is
+ * the component's minimum raster index, 0-based.  Flood
+ * fill in raster order as O1, with "same value" instead of "both nonzero". */
+int oracle_bfs_equal(const uint8_t* img, int64_t H, int64_t W, int conn, int32_t* out) {
+    int rc = check_args(img, H, W, conn, out);
+    if (rc) return rc;
+    const int64_t n = H * W;
+    for (int64_t i = 0; i < n; ++i) out[i] = -1;
+    int32_t* stack = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+    if (!stack) return O_ERR_NOMEM;
+    for (int64_t s = 0; s < n; ++s) {
+        if (out[s] >= 0) continue;
+        const uint8_t v = img[s];
+        int64_t top = 0;
+        out[s] = (int32_t)s;
+        stack[top++] = (int32_t)s;
+        while (top > 0) {
+            const int64_t p = stack[--top];
+            const int64_t y = p / W, x = p % W;
+            for (int64_t dy = -1; dy <= 1; ++dy) {
+                for (int64_t dx = -1; dx <= 1; ++dx) {
+                    if (dy == 0 && dx == 0) continue;
+                    if (conn == 4 && dy != 0 && dx != 0) continue;
+                    const int64_t yy = y + dy, xx = x + dx;
+                    if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+                    const int64_t q = yy * W + xx;
+                    if (img[q] == v && out[q] < 0) {
+                        out[q] = (int32_t)s;
+                        stack[top++] = (int32_t)q;
+                    }
+                }
+            }
+        }
+    }
+    free(stack);
+    return O_OK;
+}
+
 /* O2: sequential two-pass union-find with minimum-root union. */
 static int64_t tp_find(int32_t* parent, int64_t a) {
     while (parent[a] != a) {

@@ -15,6 +15,7 @@ from ._binding import (  # noqa: F401
     METHODS,
     MethodWorkspace,
     label_method,
+    label_equal,
     component_stats,
     STATS_FIELDS,
     StripLabeler,
@@ -32,5 +33,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "label_equal", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
            "stages", "stage_fns", "status_string", "raw"]

@@ -41,6 +41,7 @@ SIGNATURES = {
     "ccl_strip_finalize": (_int, [_vp, _int, _int, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
     "ccl_method_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int]),
     "ccl_stats_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "ccl_label_equal_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
     "ccl_component_stats_async": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ccl_label_method_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp]),
 }
@@ -195,6 +196,24 @@ def label_method(image, connectivity: int = 8, method: str = "uf", *, out=None,
         ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), METHODS[method],
         ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, _stream_ptr(stream)),
         "ccl_label_method_async")
+    return out
+
+
+def label_equal(image, connectivity: int = 8, *, out=None, stream=None):
+    """Equal-value mode (NEXT-2, ccl_label_equal_async): every pixel labeled
+    with the 0-based minimum raster index of its component of equal-valued
+    pixels (background included; grey-level input allowed)."""
+    torch = _torch()
+    _check_image(image)
+    B, H, W = _shape3(image)
+    if out is None:
+        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+    if B == 0:
+        return out
+    ws = MethodWorkspace(B, H, W, connectivity, "uf", device=image.device)
+    _check(_lib.ccl_label_equal_async(
+        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+        ws.ptr(), ws.nbytes, _stream_ptr(stream)), "ccl_label_equal_async")
     return out
 
 

@@ -489,6 +489,42 @@ size_t ccl_method_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectiv
     return 0;
 }
 
+ccl_status_t ccl_label_equal_async(const uint8_t* images, int64_t B, int64_t H, int64_t W, int connectivity,
+                                   int32_t* labels_out, void* workspace, size_t workspace_bytes, void* stream) {
+    ccl_status_t st = check_geometry(B, H, W, connectivity);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    if (B > 65535) return CCL_ERR_DIMS;
+    if (!images || !labels_out || !workspace) return CCL_ERR_NULL;
+    if (workspace_bytes < ccl_method_workspace_bytes(B, H, W, connectivity, CCL_METHOD_UF)) return CCL_ERR_WORKSPACE;
+    const size_t n = size_t(B) * size_t(H) * size_t(W);
+    if (overlaps(images, n, labels_out, n * 4) || overlaps(images, n, workspace, workspace_bytes) ||
+        overlaps(labels_out, n * 4, workspace, workspace_bytes))
+        return CCL_ERR_ALIAS;
+    namespace cb = ccl::base;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const long long npx = (long long)H * W, nn = npx * B;
+    int32_t* G = static_cast<int32_t*>(workspace);
+    const dim3 grid(unsigned((W + cb::kBX - 1) / cb::kBX), unsigned((H + cb::kBY - 1) / cb::kBY), unsigned(B));
+    const int nrows = int((H - 1) / cb::kBY), ncols = int(2 * ((W + cb::kBX - 1) / cb::kBX));
+    const long long per = (long long)nrows * W + (long long)ncols * H;
+    const unsigned flat_blocks = unsigned(std::min<long long>((nn + 255) / 256, 148LL * 16));
+    if (connectivity == 4) {
+        cb::k_uf_local<4, true><<<grid, dim3(cb::kBX, cb::kBY), 0, s>>>(images, int(H), int(W), npx, G);
+        if (per > 0)
+            cb::k_uf_global<4, true><<<dim3(unsigned((per + 255) / 256), unsigned(B)), 256, 0, s>>>(
+                images, int(H), int(W), npx, G, nrows, ncols, per);
+    } else {
+        cb::k_uf_local<8, true><<<grid, dim3(cb::kBX, cb::kBY), 0, s>>>(images, int(H), int(W), npx, G);
+        if (per > 0)
+            cb::k_uf_global<8, true><<<dim3(unsigned((per + 255) / 256), unsigned(B)), 256, 0, s>>>(
+                images, int(H), int(W), npx, G, nrows, ncols, per);
+    }
+    cb::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, labels_out, nn, npx, 0);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CCL_OK : cuda_fail(e);
+}
+
 ccl_status_t ccl_label_method_async(const uint8_t* images, int64_t B, int64_t H, int64_t W, int connectivity,
                                     int method, int32_t* labels_out, void* workspace, size_t workspace_bytes,
                                     void* stream) {

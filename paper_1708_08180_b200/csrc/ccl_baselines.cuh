@@ -77,25 +77,41 @@ __device__ __forceinline__ bool fg_at(const uint8_t* im, int W, int H, int x, in
 
 // ---------------------------------------------------------------- UF (2D)
 // Local merge: G[p] = global index of p's local root (fg), -1 (bg).
-template <int CONN>
+// EQ (equal-value mode, NEXT-2): every in-image pixel takes part and two
+// neighbours are connected iff their values are equal (the paper's raw
+// comparisons dBuff[tid] == dBuff[tid-1]); else foreground
+// (nonzero) pixels, connected iff both are foreground.
+template <bool EQ>
+__device__ __forceinline__ bool linked(const uint8_t* im, int W, int H, int x, int y, int xx, int yy) {
+    if (xx < 0 || xx >= W || yy < 0 || yy >= H) return false;
+    const uint8_t a = im[size_t(y) * W + x], c = im[size_t(yy) * W + xx];
+    return EQ ? a == c : (a != 0 && c != 0);
+}
+
+template <int CONN, bool EQ = false>
 __global__ void __launch_bounds__(kBX * kBY) k_uf_local(const uint8_t* __restrict__ img, int H, int W,
                                                         long long npx, int32_t* __restrict__ G) {
     __shared__ int32_t P[kBX * kBY];
-    __shared__ uint8_t F[kBX * kBY];
+    __shared__ uint8_t F[kBX * kBY];  // pixel value (EQ) / foreground flag
     const int b = blockIdx.z;
     const uint8_t* im = img + size_t(b) * size_t(npx);
     int32_t* Gb = G + size_t(b) * size_t(npx);
     const int lx = threadIdx.x, ly = threadIdx.y, tid = ly * kBX + lx;
     const int x = blockIdx.x * kBX + lx, y = blockIdx.y * kBY + ly;
-    const bool f = fg_at(im, W, H, x, y);
+    const bool inside = x < W && y < H;
+    const uint8_t v = inside ? im[size_t(y) * W + x] : 0;
+    const bool f = EQ ? inside : v != 0;
     P[tid] = tid;
-    F[tid] = f;
+    F[tid] = EQ ? v : uint8_t(f);
     __syncthreads();
     if (f) {
-        if (lx > 0 && F[tid - 1]) union_min(P, tid, tid - 1);
-        if (ly > 0 && F[tid - kBX]) union_min(P, tid, tid - kBX);
-        if (CONN == 8 && ly > 0 && lx > 0 && F[tid - kBX - 1]) union_min(P, tid, tid - kBX - 1);
-        if (CONN == 8 && ly > 0 && lx + 1 < kBX && F[tid - kBX + 1]) union_min(P, tid, tid - kBX + 1);
+        // in-tile neighbours (W, N, NW are inside the image whenever this
+        // pixel is; NE is checked): EQ compares values, else both foreground
+        auto m = [&](int t2) { return EQ ? F[t2] == v : F[t2] != 0; };
+        if (lx > 0 && m(tid - 1)) union_min(P, tid, tid - 1);
+        if (ly > 0 && m(tid - kBX)) union_min(P, tid, tid - kBX);
+        if (CONN == 8 && ly > 0 && lx > 0 && m(tid - kBX - 1)) union_min(P, tid, tid - kBX - 1);
+        if (CONN == 8 && ly > 0 && lx + 1 < kBX && x + 1 < W && m(tid - kBX + 1)) union_min(P, tid, tid - kBX + 1);
     }
     __syncthreads();
     if (x < W && y < H) {
@@ -113,7 +129,7 @@ __global__ void __launch_bounds__(kBX * kBY) k_uf_local(const uint8_t* __restric
 // (reading R10).  Pixel set: rows y % 16 == 0 (y > 0), then columns
 // x % 32 == 0 (x > 0) and x % 32 == 31 (x + 1 < W: the NE edge's tile
 // crossing), rows excluded from the column part to count each pixel once.
-template <int CONN>
+template <int CONN, bool EQ = false>
 __global__ void k_uf_global(const uint8_t* __restrict__ img, int H, int W, long long npx, int32_t* __restrict__ G,
                             int nrows, int ncols, long long per_img) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -133,25 +149,27 @@ __global__ void k_uf_global(const uint8_t* __restrict__ img, int H, int W, long 
     }
     const uint8_t* im = img + size_t(b) * size_t(npx);
     int32_t* Gb = G + size_t(b) * size_t(npx);
-    if (!fg_at(im, W, H, x, y)) return;
+    if (!EQ && !fg_at(im, W, H, x, y)) return;
     const int p = y * W + x;
     const bool xb = x % kBX == 0, yb = y % kBY == 0, xe = (x + 1) % kBX == 0;
-    if (xb && fg_at(im, W, H, x - 1, y)) union_min(Gb, Gb[p], Gb[p - 1]);
-    if (yb && fg_at(im, W, H, x, y - 1)) union_min(Gb, Gb[p], Gb[p - W]);
+    if (xb && linked<EQ>(im, W, H, x, y, x - 1, y)) union_min(Gb, Gb[p], Gb[p - 1]);
+    if (yb && linked<EQ>(im, W, H, x, y, x, y - 1)) union_min(Gb, Gb[p], Gb[p - W]);
     if (CONN == 8) {
-        if ((xb || yb) && fg_at(im, W, H, x - 1, y - 1)) union_min(Gb, Gb[p], Gb[p - W - 1]);
-        if ((xe || yb) && fg_at(im, W, H, x + 1, y - 1)) union_min(Gb, Gb[p], Gb[p - W + 1]);
+        if ((xb || yb) && linked<EQ>(im, W, H, x, y, x - 1, y - 1)) union_min(Gb, Gb[p], Gb[p - W - 1]);
+        if ((xe || yb) && linked<EQ>(im, W, H, x, y, x + 1, y - 1)) union_min(Gb, Gb[p], Gb[p - W + 1]);
     }
 }
 
-// Link: labels_out[p] = 1 + root (fg) or 0.
-__global__ void k_link_flat(const int32_t* __restrict__ G, int32_t* __restrict__ out, long long n, long long npx) {
+// Link: labels_out[p] = off + root (fg; off = 1, or 0 in equal-value mode)
+// or 0 (background, binary mode only).
+__global__ void k_link_flat(const int32_t* __restrict__ G, int32_t* __restrict__ out, long long n, long long npx,
+                            int off = 1) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const long long b = i / npx;
         const int32_t* Gb = G + b * npx;
         const int v = G[i];
-        out[i] = v < 0 ? 0 : find_root(Gb, v) + 1;
+        out[i] = v < 0 ? 0 : find_root(Gb, v) + off;
     }
 }
 
