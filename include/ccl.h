@@ -159,6 +159,21 @@ ccl_status_t ccl_label_equal_async(const uint8_t* images, int64_t B, int64_t H, 
                                    int connectivity, int32_t* labels_out, void* workspace,
                                    size_t workspace_bytes, void* stream);
 
+/* 3D volumes ("2D/3D grid"): B volumes of
+ * D x H x W uint8 voxels, row-major (x fastest, then y, then z; volume b at
+ * b*D*H*W), raster index (z*H + y)*W + x.  Foreground = nonzero; connectivity
+ * 6 (faces) or 26 (faces, edges, corners), clipped.  labels_out: int32, 0 or
+ * 1 + the minimum raster index of the voxel's component (per volume).  The
+ * three phases over 32x4x4 bricks at voxel granularity (csrc/ccl_3d.cuh).
+ * Workspace >= ccl_workspace_bytes_3d(...) (0 = invalid arguments).  Errors:
+ * CCL_ERR_DIMS (sizes < 1, or grid limits: B*ceil(D/4) or ceil(H/4) > 65535),
+ * CCL_ERR_TOO_LARGE (D*H*W > 2^31-1), CCL_ERR_CONNECTIVITY (not 6/26), else
+ * as ccl_label_batched_async. */
+size_t ccl_workspace_bytes_3d(int64_t B, int64_t D, int64_t H, int64_t W, int connectivity);
+ccl_status_t ccl_label_3d_async(const uint8_t* volumes, int64_t B, int64_t D, int64_t H, int64_t W,
+                                int connectivity, int32_t* labels_out, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
 /* Per-component statistics of a label map produced by ccl_label* (SURVEY.md
  * 8(f) NEXT-3; "the size and location of each dot").  For image
  * b the components are listed in increasing label order (= raster order of

@@ -16,6 +16,7 @@ Contents
 * ``label_equal``    -- equal-value mode (NEXT-2): C flood fill with "same
                         value" adjacency, every pixel labeled with its
                         component's 0-based minimum raster index.
+* ``label_3d``       -- 3D volumes (NEXT-4): C flood fill, 6- / 26-connectivity.
 * ``component_stats`` -- per-component area, bounding box and coordinate sums
                         of a canonical label map, components in increasing
                         label order ("size
@@ -70,6 +71,8 @@ def _load():
                 fn = getattr(lib, name)
                 fn.argtypes = sig
                 fn.restype = ctypes.c_int
+            lib.oracle_bfs3d.argtypes = [ctypes.c_void_p, ctypes.c_int64] + sig[1:]
+            lib.oracle_bfs3d.restype = ctypes.c_int
             lib.oracle_bfs_batched.argtypes = [ctypes.c_void_p, ctypes.c_int64] + sig[1:]
             lib.oracle_bfs_batched.restype = ctypes.c_int
             _lib = lib
@@ -113,6 +116,22 @@ def label_equal(img, connectivity: int = 8) -> np.ndarray:
     rc = _load().oracle_bfs_equal(a.ctypes.data, H, W, int(connectivity), out.ctypes.data)
     if rc:
         raise ValueError(f"oracle_bfs_equal: {ERRORS.get(rc, rc)}")
+    return out
+
+
+def label_3d(vol, connectivity: int = 26) -> np.ndarray:
+    """3D volumes (NEXT-4; "2D/3D grid"): canonical labels of a
+    D x H x W volume, 6- or 26-connectivity, raster index (z*H + y)*W + x."""
+    a = np.ascontiguousarray(np.asarray(vol))
+    if a.dtype != np.uint8:
+        a = np.ascontiguousarray((a != 0).astype(np.uint8))
+    if a.ndim != 3:
+        raise ValueError("expected a 3D volume [D,H,W]")
+    D, H, W = a.shape
+    out = np.empty((D, H, W), dtype=np.int32)
+    rc = _load().oracle_bfs3d(a.ctypes.data, D, H, W, int(connectivity), out.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_bfs3d: {ERRORS.get(rc, rc)}")
     return out
 
 

@@ -126,6 +126,48 @@ int oracle_bfs_equal(const uint8_t* img, int64_t H, int64_t W, int conn, int32_t
     return O_OK;
 }
 
+/* 3D volumes ("2D/3D grid"): voxel
+ * (x,y,z) of a D x H x W volume has raster index (z*H + y)*W + x; foreground
+ * = nonzero; 6-connectivity (faces) or 26-connectivity (faces, edges,
+ * corners), clipped; label = 0 or 1 + the component's minimum raster index.
+ * Flood fill seeded in raster order, as O1. */
+int oracle_bfs3d(const uint8_t* vol, int64_t D, int64_t H, int64_t W, int conn, int32_t* out) {
+    if (!vol || !out) return O_ERR_NULL;
+    if (D < 1 || H < 1 || W < 1) return O_ERR_DIMS;
+    if (H * W > INT32_MAX / D) return O_ERR_TOO_LARGE;
+    if (conn != 6 && conn != 26) return O_ERR_CONN;
+    const int64_t n = D * H * W;
+    memset(out, 0, (size_t)n * sizeof(int32_t));
+    int32_t* stack = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+    if (!stack) return O_ERR_NOMEM;
+    for (int64_t s = 0; s < n; ++s) {
+        if (vol[s] == 0 || out[s] != 0) continue;
+        const int32_t lab = (int32_t)(s + 1);
+        int64_t top = 0;
+        out[s] = lab;
+        stack[top++] = (int32_t)s;
+        while (top > 0) {
+            const int64_t p = stack[--top];
+            const int64_t z = p / (H * W), y = (p / W) % H, x = p % W;
+            for (int64_t dz = -1; dz <= 1; ++dz)
+                for (int64_t dy = -1; dy <= 1; ++dy)
+                    for (int64_t dx = -1; dx <= 1; ++dx) {
+                        const int64_t nz = (dz != 0) + (dy != 0) + (dx != 0);
+                        if (nz == 0 || (conn == 6 && nz != 1)) continue;
+                        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+                        if (zz < 0 || zz >= D || yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+                        const int64_t q = (zz * H + yy) * W + xx;
+                        if (vol[q] != 0 && out[q] == 0) {
+                            out[q] = lab;
+                            stack[top++] = (int32_t)q;
+                        }
+                    }
+        }
+    }
+    free(stack);
+    return O_OK;
+}
+
 /* O2: sequential two-pass union-find with minimum-root union. */
 static int64_t tp_find(int32_t* parent, int64_t a) {
     while (parent[a] != a) {

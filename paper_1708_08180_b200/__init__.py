@@ -16,6 +16,7 @@ from ._binding import (  # noqa: F401
     MethodWorkspace,
     label_method,
     label_equal,
+    label_3d,
     component_stats,
     STATS_FIELDS,
     StripLabeler,
@@ -33,5 +34,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "label_equal", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
            "stages", "stage_fns", "status_string", "raw"]

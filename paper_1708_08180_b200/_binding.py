@@ -42,6 +42,8 @@ SIGNATURES = {
     "ccl_method_workspace_bytes": (_sz, [_i64, _i64, _i64, _int, _int]),
     "ccl_stats_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "ccl_label_equal_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
+    "ccl_workspace_bytes_3d": (_sz, [_i64, _i64, _i64, _i64, _int]),
+    "ccl_label_3d_async": (_int, [_vp, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
     "ccl_component_stats_async": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ccl_label_method_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp]),
 }
@@ -214,6 +216,30 @@ def label_equal(image, connectivity: int = 8, *, out=None, stream=None):
     _check(_lib.ccl_label_equal_async(
         ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
         ws.ptr(), ws.nbytes, _stream_ptr(stream)), "ccl_label_equal_async")
+    return out
+
+
+def label_3d(volume, connectivity: int = 26, *, out=None, stream=None):
+    """3D volumes (NEXT-4, ccl_label_3d_async): uint8 CUDA [D,H,W] or
+    [B,D,H,W], 6- or 26-connectivity -> int32 labels (0 or 1 + minimum raster
+    index (z*H + y)*W + x of the component)."""
+    torch = _torch()
+    _check_image(volume)
+    if volume.dim() == 3:
+        B, (D, H, W) = 1, volume.shape
+    elif volume.dim() == 4:
+        B, D, H, W = volume.shape
+    else:
+        raise ValueError("expected [D,H,W] or [B,D,H,W]")
+    if out is None:
+        out = torch.empty(volume.shape, dtype=torch.int32, device=volume.device)
+    if B == 0:
+        return out
+    n = int(_lib.ccl_workspace_bytes_3d(B, D, H, W, int(connectivity)))
+    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=volume.device)
+    _check(_lib.ccl_label_3d_async(
+        ctypes.c_void_p(volume.data_ptr()), B, D, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+        ctypes.c_void_p(ws.data_ptr()), n, _stream_ptr(stream)), "ccl_label_3d_async")
     return out
 
 

@@ -5,6 +5,7 @@
 #include "ccl_strip.cuh"
 #include "ccl_baselines.cuh"
 #include "ccl_stats.cuh"
+#include "ccl_3d.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -521,6 +522,46 @@ ccl_status_t ccl_label_equal_async(const uint8_t* images, int64_t B, int64_t H, 
                 images, int(H), int(W), npx, G, nrows, ncols, per);
     }
     cb::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, labels_out, nn, npx, 0);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CCL_OK : cuda_fail(e);
+}
+
+size_t ccl_workspace_bytes_3d(int64_t B, int64_t D, int64_t H, int64_t W, int connectivity) {
+    if (B < 0 || D < 1 || H < 1 || W < 1 || (connectivity != 6 && connectivity != 26)) return 0;
+    if (H > INT32_MAX / W || H * W > INT32_MAX / D) return 0;
+    return align_up(size_t(B) * size_t(D) * size_t(H) * size_t(W) * sizeof(int32_t));
+}
+
+ccl_status_t ccl_label_3d_async(const uint8_t* volumes, int64_t B, int64_t D, int64_t H, int64_t W,
+                                int connectivity, int32_t* labels_out, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+    if (B < 0 || D < 1 || H < 1 || W < 1) return CCL_ERR_DIMS;
+    if (H > INT32_MAX / W || H * W > INT32_MAX / D) return CCL_ERR_TOO_LARGE;
+    if (connectivity != 6 && connectivity != 26) return CCL_ERR_CONNECTIVITY;
+    if (B == 0) return CCL_OK;
+    namespace cv = ccl::vol;
+    const long long bz = (D + cv::kZ - 1) / cv::kZ;
+    if (B * bz > 65535 || B > 65535 || (H + cv::kY - 1) / cv::kY > 65535) return CCL_ERR_DIMS;  // grid limits
+    if (!volumes || !labels_out || !workspace) return CCL_ERR_NULL;
+    if (workspace_bytes < ccl_workspace_bytes_3d(B, D, H, W, connectivity)) return CCL_ERR_WORKSPACE;
+    const long long nvox = D * H * W, n = nvox * B;
+    if (overlaps(volumes, size_t(n), labels_out, size_t(n) * 4) || overlaps(volumes, size_t(n), workspace, workspace_bytes) ||
+        overlaps(labels_out, size_t(n) * 4, workspace, workspace_bytes))
+        return CCL_ERR_ALIAS;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t* G = static_cast<int32_t*>(workspace);
+    const dim3 grid(unsigned((W + cv::kX - 1) / cv::kX), unsigned((H + cv::kY - 1) / cv::kY), unsigned(B * bz));
+    const dim3 blk(cv::kX, cv::kY, cv::kZ);
+    const dim3 gb(unsigned((nvox + 255) / 256), unsigned(B));
+    if (connectivity == 6) {
+        cv::k_vol_local<6><<<grid, blk, 0, s>>>(volumes, int(D), int(H), int(W), nvox, int(bz), G);
+        cv::k_vol_boundary<6><<<gb, 256, 0, s>>>(volumes, int(D), int(H), int(W), nvox, G);
+    } else {
+        cv::k_vol_local<26><<<grid, blk, 0, s>>>(volumes, int(D), int(H), int(W), nvox, int(bz), G);
+        cv::k_vol_boundary<26><<<gb, 256, 0, s>>>(volumes, int(D), int(H), int(W), nvox, G);
+    }
+    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, 148LL * 16));
+    ccl::base::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, labels_out, n, nvox, 1);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
 }
