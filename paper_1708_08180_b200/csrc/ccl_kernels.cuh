@@ -382,10 +382,16 @@ struct __align__(16) WordE {
 // to the scratch path).  A tile with more runs (period-2 stripes,
 // checkerboards: up to TY*512) keeps them in the block's slot of a global
 // scratch area instead (same code, L2-resident).
+#ifndef CCL_K1_CAP16
+#define CCL_K1_CAP16 4576
+#endif
+#ifndef CCL_K1_BLOCKS
+#define CCL_K1_BLOCKS 5
+#endif
 template <int TY>
 __host__ __device__ constexpr int k1_cap() {
     // TY = 32: 16 KB of row words; 3456 runs keep the block at 44 KB (5 per SM)
-    return TY * kTileW / 2 < (TY > 16 ? 3456 : 4576) ? TY * kTileW / 2 : (TY > 16 ? 3456 : 4576);
+    return TY * kTileW / 2 < (TY > 16 ? 3456 : CCL_K1_CAP16) ? TY * kTileW / 2 : (TY > 16 ? 3456 : CCL_K1_CAP16);
 }
 template <int TY>
 __host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
@@ -1018,7 +1024,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads1, 5) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+__global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              int32_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
