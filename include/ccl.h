@@ -66,9 +66,11 @@ int ccl_last_cuda_error(void);
 
 /* Device workspace (bytes) needed by the *_async entry points for B images of
  * H x W: the global union-find parent array of the boundary analysis (one int32
- * per pixel, only tile-edge entries are ever touched) plus the bit-packed
- * foreground mask (one bit per pixel, rows padded to 32 px).  Returns 0 for
- * invalid arguments. */
+ * per pixel, only tile-edge entries are ever touched), the bit-packed
+ * foreground mask (one bit per pixel, rows padded to 32 px), per-run records,
+ * per-tile edge blocks and resolved labels, and the K1 scratch slots for
+ * run-dense tiles.  Sized for every tile configuration.
+ * Returns 0 for invalid arguments. */
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
 
 /* Label one H x W image (device pointers).  Allocates its workspace stream-
@@ -94,7 +96,9 @@ ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H
                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* As ccl_label_batched_async with an explicit tile height (rows per K1 thread
- * block: 8, 16 or 32; 0 = library default).  The tile width is fixed at 1024
+ * block: 8, 16 or 32; 0 = library default: 16, or 8 when 16-row tiles would
+ * number fewer than 592 = 148 SMs x 4, i.e. small images; CCL_TILE_AUTO=0 in
+ * the environment pins the default to 16).  The tile width is fixed at 1024
  * pixels (32 lanes x 32 px).  Output is identical for every tile config
  * ("config independence"); unsupported values -> CCL_ERR_CONFIG. */
 ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
