@@ -800,7 +800,10 @@ __device__ __forceinline__ size_t tile_index(const Geom& g, int b, int ty, int t
 }
 
 // The horizontal boundary above tile (b, band >= 1, tx); one warp.
-constexpr int kPairsPerLane = 4;  // boundary pairs a lane contributes per round
+#ifndef CCL_PAIRS_PER_LANE
+#define CCL_PAIRS_PER_LANE 4
+#endif
+constexpr int kPairsPerLane = CCL_PAIRS_PER_LANE;  // boundary pairs a lane contributes per round
 
 template <int TY, int CONN, bool NOUNION = false>
 __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
