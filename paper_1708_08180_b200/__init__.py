@@ -12,6 +12,7 @@ CUDA behind the C ABI in include/ccl.h); this package only marshals arguments.
 from ._binding import (  # noqa: F401
     CCLError,
     HostSession,
+    HostPipeline,
     METHODS,
     MethodWorkspace,
     label_method,
@@ -34,5 +35,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "HostPipeline", "CCLError", "workspace_bytes", "boundary_work_items",
            "stages", "stage_fns", "status_string", "raw"]

@@ -344,6 +344,29 @@ class HostSession:
         return 4 * self.B * self.H * self.W
 
 
+class HostPipeline:
+    """End-to-end labeling of a stream of host images: ``depth`` HostSessions
+    (pinned host buffers + device scratch) on ``depth`` CUDA streams, used
+    round-robin, so that step i's device->host copy of its labels overlaps
+    step i+1's host->device copy and kernels (PCIe is full duplex).  Every
+    step still copies its own image in and its own labels out through
+    ccl_label_host_async."""
+
+    def __init__(self, B: int, H: int, W: int, connectivity: int = 8, depth: int = 2):
+        torch = _torch()
+        self.sessions = [HostSession(B, H, W, connectivity) for _ in range(depth)]
+        self.streams = [torch.cuda.Stream() for _ in range(depth)]
+
+    def enqueue(self, i: int):
+        """Enqueue step i (no synchronisation); returns its session."""
+        sess, st = self.sessions[i % len(self.sessions)], self.streams[i % len(self.streams)]
+        _check(_lib.ccl_label_host_async(
+            ctypes.c_void_p(sess.h_image.data_ptr()), sess.B, sess.H, sess.W, sess.conn,
+            ctypes.c_void_p(sess.h_labels.data_ptr()), ctypes.c_void_p(sess.scratch.data_ptr()),
+            sess.scratch_bytes, ctypes.c_void_p(st.cuda_stream)), "ccl_label_host_async")
+        return sess
+
+
 # ------------------------------------------------------------- strip sharding
 class StripLabeler:
     """Row-strip sharded labeling of one H_total x W image: this object owns

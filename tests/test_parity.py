@@ -273,6 +273,20 @@ def test_host_session_e2e(ccl):
     assert_same(got, oracle.label_bfs_batched(imgs, 8), "host e2e")
 
 
+def test_host_pipeline_e2e(ccl):
+    # two sessions on two streams, steps enqueued back to back without syncs
+    import torch
+    imgs = [synth.noise(300, 700, 0.5, seed=11), synth.blobs(300, 700, seed=12)]
+    pipe = ccl.HostPipeline(1, 300, 700, 8, depth=2)
+    for sess, im in zip(pipe.sessions, imgs):
+        sess.h_image.copy_(torch.from_numpy(im[None]))
+    for i in range(6):
+        pipe.enqueue(i)
+    torch.cuda.synchronize()
+    for sess, im in zip(pipe.sessions, imgs):
+        assert_same(sess.h_labels.numpy()[0], oracle.label_bfs(im, 8), "host pipeline")
+
+
 def test_degenerate(ccl):
     import torch
     for H, W in [(1, 1), (1, 2), (2, 1), (1, 1025), (1025, 1)]:
