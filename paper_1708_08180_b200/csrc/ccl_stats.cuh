@@ -264,6 +264,21 @@ __global__ void __launch_bounds__(kT) k_stats_accum(const int32_t* __restrict__ 
             sx0 -= W;
             ++sy0;
         }
+        // fast paths: an all-background segment, and a segment lying wholly in
+        // one row of the component carried in registers
+        const unsigned bgm = __ballot_sync(0xFFFFFFFFu, cid < 0);
+        if (bgm == 0xFFFFFFFFu) continue;
+        const int y_first = __shfl_sync(0xFFFFFFFFu, y, 0), x_first = __shfl_sync(0xFFFFFFFFu, x, 0);
+        if (acid >= 0 && __all_sync(0xFFFFFFFFu, cid == acid && y == y_first)) {
+            aarea += 32;
+            ax0 = min(ax0, x_first);
+            ax1 = max(ax1, x_first + 31);
+            ay0 = min(ay0, y_first);
+            ay1 = max(ay1, y_first);
+            asx += 32ull * unsigned(x_first) + 496ull;
+            asy += 32ull * unsigned(y_first);
+            continue;
+        }
         // runs of equal (component, row) along the segment: every statistic
         // of a run is a closed form of its first x and its length
         const int pc = __shfl_up_sync(0xFFFFFFFFu, cid, 1), py = __shfl_up_sync(0xFFFFFFFFu, y, 1);
