@@ -67,11 +67,13 @@ def corpus(seed=21):
     yield "empty", np.zeros((50, 2100), np.uint8)
 
 
+@pytest.mark.parametrize("tile_rows", [0, 16])  # 0: default rule (8-row tiles for these small images)
 @pytest.mark.parametrize("conn", CONNS)
-def test_corpus(ccl, conn):
+def test_corpus(ccl, conn, tile_rows):
     n = 0
     for name, img in corpus():
-        assert_same(gpu_label(ccl, img, conn), oracle.label_bfs(img, conn), f"{name} conn{conn}")
+        assert_same(gpu_label(ccl, img, conn, tile_rows=tile_rows), oracle.label_bfs(img, conn),
+                    f"{name} conn{conn} tile_rows={tile_rows}")
         n += 1
     assert n >= 500
 
