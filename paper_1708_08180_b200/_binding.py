@@ -8,6 +8,7 @@ loaded, importing this module raises (build it with
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -116,6 +117,37 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+@contextlib.contextmanager
+def _on(device, stream=None):
+    """Run a wrapper body on ``device``: it becomes the current device (the
+    library launches on the current device), ``stream`` defaults to that
+    device's current stream, and every temporary the body allocates belongs to
+    that stream in the caching allocator (so a block is not handed to another
+    stream while the library's kernels still use it)."""
+    torch = _torch()
+    device = torch.device(device)
+    with torch.cuda.device(device):
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        if s.device != device:
+            raise ValueError(f"stream is on {s.device}, the tensors on {device}")
+        with torch.cuda.stream(s):
+            yield s
+
+
+def _same_device(device, *tensors):
+    for t in tensors:
+        if t is not None and t.device != device:
+            raise ValueError(f"all tensors must be on {device}, got one on {t.device}")
+
+
+def _check_out(out, shape, device):
+    """A caller-supplied output: contiguous int32 of the input's shape, same device."""
+    torch = _torch()
+    if out.dtype != torch.int32 or tuple(out.shape) != tuple(shape) or not out.is_contiguous():
+        raise ValueError("out must be a contiguous int32 tensor of the input's shape")
+    _same_device(device, out)
+
+
 def _check_image(image):
     torch = _torch()
     if not isinstance(image, torch.Tensor) or not image.is_cuda:
@@ -149,17 +181,19 @@ def label(image, connectivity: int = 8, *, out=None, workspace: Workspace | None
     torch = _torch()
     _check_image(image)
     B, H, W = _shape3(image)
-    if out is None:
-        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
-    elif out.dtype != torch.int32 or out.shape != image.shape or not out.is_contiguous():
-        raise ValueError("out must be a contiguous int32 tensor of the image's shape")
-    if B == 0:
-        return out
-    if workspace is None:
-        workspace = Workspace(B, H, W, connectivity, device=image.device)
-    _check(_lib.ccl_label_batched_cfg_async(
-        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
-        workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(stream)), "ccl_label_batched_cfg_async")
+    with _on(image.device, stream) as s:
+        if out is None:
+            out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+        else:
+            _check_out(out, image.shape, image.device)
+        if B == 0:
+            return out
+        if workspace is None:
+            workspace = Workspace(B, H, W, connectivity, device=image.device)
+        _same_device(image.device, workspace.buf)
+        _check(_lib.ccl_label_batched_cfg_async(
+            ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+            workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(s)), "ccl_label_batched_cfg_async")
     return out
 
 
@@ -188,16 +222,20 @@ def label_method(image, connectivity: int = 8, method: str = "uf", *, out=None,
     B, H, W = _shape3(image)
     if method not in METHODS:
         raise ValueError(f"method must be one of {sorted(METHODS)}")
-    if out is None:
-        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
-    if B == 0:
-        return out
-    if workspace is None:
-        workspace = MethodWorkspace(B, H, W, connectivity, method, device=image.device)
-    _check(_lib.ccl_label_method_async(
-        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), METHODS[method],
-        ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, _stream_ptr(stream)),
-        "ccl_label_method_async")
+    with _on(image.device, stream) as s:
+        if out is None:
+            out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+        else:
+            _check_out(out, image.shape, image.device)
+        if B == 0:
+            return out
+        if workspace is None:
+            workspace = MethodWorkspace(B, H, W, connectivity, method, device=image.device)
+        _same_device(image.device, workspace.buf)
+        _check(_lib.ccl_label_method_async(
+            ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), METHODS[method],
+            ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, _stream_ptr(s)),
+            "ccl_label_method_async")
     return out
 
 
@@ -208,14 +246,17 @@ def label_equal(image, connectivity: int = 8, *, out=None, stream=None):
     torch = _torch()
     _check_image(image)
     B, H, W = _shape3(image)
-    if out is None:
-        out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
-    if B == 0:
-        return out
-    ws = MethodWorkspace(B, H, W, connectivity, "uf", device=image.device)
-    _check(_lib.ccl_label_equal_async(
-        ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
-        ws.ptr(), ws.nbytes, _stream_ptr(stream)), "ccl_label_equal_async")
+    with _on(image.device, stream) as s:
+        if out is None:
+            out = torch.empty(image.shape, dtype=torch.int32, device=image.device)
+        else:
+            _check_out(out, image.shape, image.device)
+        if B == 0:
+            return out
+        ws = MethodWorkspace(B, H, W, connectivity, "uf", device=image.device)
+        _check(_lib.ccl_label_equal_async(
+            ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+            ws.ptr(), ws.nbytes, _stream_ptr(s)), "ccl_label_equal_async")
     return out
 
 
@@ -231,15 +272,18 @@ def label_3d(volume, connectivity: int = 26, *, out=None, stream=None):
         B, D, H, W = volume.shape
     else:
         raise ValueError("expected [D,H,W] or [B,D,H,W]")
-    if out is None:
-        out = torch.empty(volume.shape, dtype=torch.int32, device=volume.device)
-    if B == 0:
-        return out
-    n = int(_lib.ccl_workspace_bytes_3d(B, D, H, W, int(connectivity)))
-    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=volume.device)
-    _check(_lib.ccl_label_3d_async(
-        ctypes.c_void_p(volume.data_ptr()), B, D, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
-        ctypes.c_void_p(ws.data_ptr()), n, _stream_ptr(stream)), "ccl_label_3d_async")
+    with _on(volume.device, stream) as s:
+        if out is None:
+            out = torch.empty(volume.shape, dtype=torch.int32, device=volume.device)
+        else:
+            _check_out(out, volume.shape, volume.device)
+        if B == 0:
+            return out
+        n = int(_lib.ccl_workspace_bytes_3d(B, D, H, W, int(connectivity)))
+        ws = torch.empty(max(n, 1), dtype=torch.uint8, device=volume.device)
+        _check(_lib.ccl_label_3d_async(
+            ctypes.c_void_p(volume.data_ptr()), B, D, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(ws.data_ptr()), n, _stream_ptr(s)), "ccl_label_3d_async")
     return out
 
 
@@ -260,14 +304,15 @@ def component_stats(labels, max_components: int | None = None, stream=None):
     B, H, W = _shape3(labels)
     if max_components is None:
         max_components = (H * W + 1) // 2 + 1  # 4-conn checkerboard bound
-    rec = torch.empty((max(B, 1), max_components, 40), dtype=torch.uint8, device=labels.device)
-    counts = torch.zeros(max(B, 1), dtype=torch.int32, device=labels.device)
-    ws_n = int(_lib.ccl_stats_workspace_bytes(B, H, W))
-    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=labels.device)
-    _check(_lib.ccl_component_stats_async(
-        ctypes.c_void_p(labels.data_ptr()), B, H, W, int(max_components), ctypes.c_void_p(rec.data_ptr()),
-        ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws_n, _stream_ptr(stream)),
-        "ccl_component_stats_async")
+    with _on(labels.device, stream) as s:
+        rec = torch.empty((max(B, 1), max_components, 40), dtype=torch.uint8, device=labels.device)
+        counts = torch.zeros(max(B, 1), dtype=torch.int32, device=labels.device)
+        ws_n = int(_lib.ccl_stats_workspace_bytes(B, H, W))
+        ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=labels.device)
+        _check(_lib.ccl_component_stats_async(
+            ctypes.c_void_p(labels.data_ptr()), B, H, W, int(max_components), ctypes.c_void_p(rec.data_ptr()),
+            ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws_n, _stream_ptr(s)),
+            "ccl_component_stats_async")
     i32 = rec.view(torch.int32)  # [B, max, 10]
     i64 = rec.view(torch.int64)  # [B, max, 5]
     out = {f: i32[..., k] for k, f in enumerate(STATS_FIELDS[:6])}
@@ -279,6 +324,7 @@ def component_stats(labels, max_components: int | None = None, stream=None):
 def stages(image, connectivity: int, out, workspace: Workspace, tile_rows: int = 0, stream=None):
     """Enqueue K1, K2, K3 as three separate C-ABI calls (per-kernel timing)."""
     B, H, W = _shape3(image)
+    _same_device(image.device, out, workspace.buf)
     s = _stream_ptr(stream)
     ws = workspace.ptr()
     _check(_lib.ccl_stage_local_merge(ctypes.c_void_p(image.data_ptr()), B, H, W, connectivity, ws,
@@ -389,18 +435,22 @@ class StripLabeler:
 
     def local(self, strip, stream=None):
         _check_image(strip)
-        _check(_lib.ccl_strip_local(ctypes.c_void_p(strip.data_ptr()), self.rows, self.W, self.row0, self.H,
-                                    self.conn, self.k, ctypes.c_void_p(self.send.data_ptr()),
-                                    ctypes.c_void_p(self.out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()),
-                                    self.ws_bytes, _stream_ptr(stream)), "ccl_strip_local")
+        _same_device(self.ws.device, strip)
+        with _on(self.ws.device, stream) as s:
+            _check(_lib.ccl_strip_local(ctypes.c_void_p(strip.data_ptr()), self.rows, self.W, self.row0, self.H,
+                                        self.conn, self.k, ctypes.c_void_p(self.send.data_ptr()),
+                                        ctypes.c_void_p(self.out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()),
+                                        self.ws_bytes, _stream_ptr(s)), "ccl_strip_local")
         return self.send
 
     def finalize(self, gathered=None, stream=None):
         g = self.gathered if gathered is None else gathered
-        _check(_lib.ccl_strip_finalize(ctypes.c_void_p(g.data_ptr()), self.k, self.rank, self.rows, self.W,
-                                       self.row0, self.H, self.conn, ctypes.c_void_p(self.out.data_ptr()),
-                                       ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream_ptr(stream)),
-               "ccl_strip_finalize")
+        _same_device(self.ws.device, g)
+        with _on(self.ws.device, stream) as s:
+            _check(_lib.ccl_strip_finalize(ctypes.c_void_p(g.data_ptr()), self.k, self.rank, self.rows, self.W,
+                                           self.row0, self.H, self.conn, ctypes.c_void_p(self.out.data_ptr()),
+                                           ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes, _stream_ptr(s)),
+                   "ccl_strip_finalize")
         return self.out
 
     def label(self, strip, group=None):

@@ -109,37 +109,53 @@ template <int TY>
 size_t smem_bytes_k1() { return sizeof(ccl::K1Smem<TY>); }
 
 template <int TY, int CONN, bool VEC>
-cudaError_t setup_attrs() {
-    // opt in to > 48 KB dynamic shared memory once per instantiation
-    static cudaError_t once = [] {
+cudaError_t setup_attrs_now() {
 #ifndef CCL_K2_CARVEOUT
 #define CCL_K2_CARVEOUT 40
 #endif
-        // K2's finds are served from L1 (ld.global.ca): a 40 % shared-memory
-        // carveout (100 KB: 5-6 resident 16 KB blocks) leaves the rest of the
-        // 256 KB to L1.  Measured, C3 K2 µs: default (no hint) 26-29 and
-        // varying between runs, 100 % 25, 40 % 24.5, 0 % 49 (blocks no
-        // longer all resident); noise 80 / 65 / 56 / 149.
-        cudaFuncSetAttribute(ccl::k_boundary<TY, CONN>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             CCL_K2_CARVEOUT);
-        cudaError_t e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem_bytes_k1<TY>()));
-        if (e != cudaSuccess) return e;
-        const int sm3 = int(smem_bytes<TY>());
-        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
-            return e;
-        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
-            return e;
-        if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
-            return e;
-        return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
-    }();
-    return once;
+    // K2's finds are served from L1 (ld.global.ca): a 40 % shared-memory
+    // carveout (100 KB: 5-6 resident 16 KB blocks) leaves the rest of the
+    // 256 KB to L1.  Measured, C3 K2 µs: default (no hint) 26-29 and
+    // varying between runs, 100 % 25, 40 % 24.5, 0 % 49 (blocks no
+    // longer all resident); noise 80 / 65 / 56 / 149.
+    cudaFuncSetAttribute(ccl::k_boundary<TY, CONN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         CCL_K2_CARVEOUT);
+    cudaError_t e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem_bytes_k1<TY>()));
+    if (e != cudaSuccess) return e;
+    const int sm3 = int(smem_bytes<TY>());
+    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
+}
+
+// Kernel attributes (> 48 KB dynamic shared memory opt-in, carveout) are
+// per device: applied once per instantiation AND device (the current one).
+template <int TY, int CONN, bool VEC>
+cudaError_t setup_attrs() {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static bool done[kMaxDev] = {false};
+    static cudaError_t result[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return setup_attrs_now<TY, CONN, VEC>();
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done[dev]) {
+        result[dev] = setup_attrs_now<TY, CONN, VEC>();
+        done[dev] = true;
+    }
+    return result[dev];
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -397,7 +413,9 @@ ccl_status_t validate_buffers(const Plan& p, const uint8_t* img, const int32_t* 
     if ((stages & kK3) && !out) return CCL_ERR_NULL;
     if (!ws) return CCL_ERR_NULL;
     if (ws_bytes < p.total()) return CCL_ERR_WORKSPACE;
-    if (reinterpret_cast<uintptr_t>(ws) % 4) return CCL_ERR_WORKSPACE;
+    // 256-byte aligned (include/ccl.h): the kernels use 16-byte vector
+    // accesses into the workspace regions, which are 256-byte multiples
+    if (reinterpret_cast<uintptr_t>(ws) % kAlign) return CCL_ERR_WORKSPACE;
     if (img && out && overlaps(img, n, out, n * sizeof(int32_t))) return CCL_ERR_ALIAS;
     if (img && overlaps(img, n, ws, ws_bytes)) return CCL_ERR_ALIAS;
     if (out && overlaps(out, n * sizeof(int32_t), ws, ws_bytes)) return CCL_ERR_ALIAS;

@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kT) k_stats_rank(const int32_t* __restrict__ l
     ccl_component_t* O = out + size_t(b) * size_t(max_components);
     const long long base = (long long)c * kChunk + (long long)threadIdx.x * (kChunk / kT);  // 16 consecutive px
     unsigned flags = 0;
-    if (base + kChunk / kT <= npx && (npx & 3) == 0) {  // 4 x 16-byte loads (rows of images are 16-B aligned here)
+    if (base + kChunk / kT <= npx && (npx & 3) == 0 && (reinterpret_cast<uintptr_t>(labels) & 15) == 0) {
+        // 4 x 16-byte loads (16-B aligned: aligned base, npx % 4 == 0); else scalar
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int4 v = __ldcs(reinterpret_cast<const int4*>(L + base) + q);

@@ -73,8 +73,12 @@ def test_validation_codes(ccl):
     need = ccl.workspace_bytes(1, 64, 64, conn)
     assert L.ccl_label_batched_async(FAKE_A, 1, 64, 64, conn, FAKE_B, FAKE_WS, need - 1, None) == 6
     # workspace overlapping the image
-    assert L.ccl_label_batched_async(FAKE_A, 1, 64, 64, conn, FAKE_B, ctypes.c_void_p(0x10000000 - 16),
+    assert L.ccl_label_batched_async(FAKE_A, 1, 64, 64, conn, FAKE_B, ctypes.c_void_p(0x10000000 - 256),
                                      need, None) == 5
+    # workspace not 256-byte aligned (include/ccl.h; the kernels use 16-byte vector accesses)
+    for off in (4, 8, 16, 128):
+        assert L.ccl_label_batched_async(FAKE_A, 1, 64, 64, conn, FAKE_B, ctypes.c_void_p(0x30000000 + off),
+                                         need, None) == 6
     # unsupported tile config
     assert L.ccl_label_batched_cfg_async(FAKE_A, 1, 64, 64, conn, FAKE_B, FAKE_WS, need, 7, None) == 8
     # B == 0 is a no-op

@@ -173,7 +173,7 @@ int main(int argc, char** argv) {
             CK(cudaMemsetAsync(flush, i, fb));
             k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
             CK(cudaEventRecord(a));
-            k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
+            k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
             CK(cudaEventRecord(b));
             CK(cudaEventSynchronize(b));
             float ms;
