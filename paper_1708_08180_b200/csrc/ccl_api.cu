@@ -73,6 +73,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.label_off = 0;
     p.g.force_top = 0;
     p.g.force_bottom = 0;
+    p.g.k3_early = 1;
     p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
     // per-run records: capacity of the worst case (alternating pixels) for the
@@ -105,6 +106,12 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 
 template <int TY>
 size_t smem_bytes() { return sizeof(ccl::LinkSmem<TY>); }
+
+// the K3 kernel (TMA row stores / resolve in the helper warp)
+template <int TY, int CONN, bool VEC, bool TMA, bool RES>
+constexpr auto k3_kernel() {
+    return ccl::k_link<TY, CONN, VEC, TMA, RES>;
+}
 template <int TY>
 size_t smem_bytes_k1() { return sizeof(ccl::K1Smem<TY>); }
 
@@ -125,16 +132,16 @@ cudaError_t setup_attrs_now() {
                                          int(smem_bytes_k1<TY>()));
     if (e != cudaSuccess) return e;
     const int sm3 = int(smem_bytes<TY>());
-    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, true>,
+    if ((e = cudaFuncSetAttribute(k3_kernel<TY, CONN, VEC, false, true>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, true>,
+    if ((e = cudaFuncSetAttribute(k3_kernel<TY, CONN, VEC, true, true>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, false, false>,
+    if ((e = cudaFuncSetAttribute(k3_kernel<TY, CONN, VEC, false, false>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
         return e;
-    return cudaFuncSetAttribute(ccl::k_link<TY, CONN, VEC, true, false>,
+    return cudaFuncSetAttribute(k3_kernel<TY, CONN, VEC, true, false>(),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
 }
 
@@ -236,7 +243,7 @@ int persistent_blocks(int which) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads1,
                                                       smem_bytes_k1<TY>());
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_link<TY, CONN, VEC, true, true>, ccl::kK3Threads,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_kernel<TY, CONN, VEC, true, true>(), ccl::kK3Threads,
                                                       smem_bytes<TY>());
     cached[w][dev] = std::max(1, sms) * std::max(1, b);
     return cached[w][dev];
@@ -278,7 +285,11 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
             // warp, ~5900 warps resident in one wave)
             int sub_log2 = 0;
             while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= 148LL * 40) ++sub_log2;
-            e = launch_pdl(ccl::k_boundary<TY, CONN>, unsigned(((n_h << sub_log2) + n_v + 7) / 8), 256, 0, s, g,
+#ifndef CCL_K2_DBG
+#define CCL_K2_DBG 0  // timing experiments only (tools/build_variant.sh): 3 = skip K2, 4 = no unions
+#endif
+            e = launch_pdl(ccl::k_boundary<TY, CONN, CCL_K2_DBG>,
+                           unsigned(((n_h << sub_log2) + n_v + 7) / 8), 256, 0, s, g,
                            (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v, sub_log2);
             if (e != cudaSuccess) return e;
         }
@@ -312,6 +323,15 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK3) {
+        // K3 reads K1's outputs before its PDL wait unless K1 is its direct
+        // predecessor in this call (an image with a single tile: no boundaries)
+        ccl::Geom g3 = g;
+        if ((stages & kK1) && !(stages & kStripFinalize)) {
+            const long long nb = (long long)g.B * (g.tiles_y - 1) * g.tiles_x +
+                                 (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
+                                     (g.tiles_x - 1);
+            g3.k3_early = nb > 0;
+        }
         // labels leave through TMA bulk-tensor stores when rows are 32-px
         // multiples (all bench configs); else 128-bit st.global.cs.  The
         // helper warp resolves the edge roots (RES), or in strip mode takes
@@ -320,9 +340,9 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         std::memset(&map, 0, sizeof(map));
         const bool tma = VEC && g.W % 32 == 0 && encode_label_map(&map, out, g);
         const bool res = !(stages & kStripFinalize);
-        auto k3 = tma ? (res ? ccl::k_link<TY, CONN, VEC, true, true> : ccl::k_link<TY, CONN, VEC, true, false>)
-                      : (res ? ccl::k_link<TY, CONN, VEC, false, true> : ccl::k_link<TY, CONN, VEC, false, false>);
-        e = launch_pdl(k3, grid3, ccl::kK3Threads, smem, s, g, (const uint32_t*)bits, (const uint32_t*)runs,
+        auto k3 = tma ? (res ? k3_kernel<TY, CONN, VEC, true, true>() : k3_kernel<TY, CONN, VEC, true, false>())
+                      : (res ? k3_kernel<TY, CONN, VEC, false, true>() : k3_kernel<TY, CONN, VEC, false, false>());
+        e = launch_pdl(k3, grid3, ccl::kK3Threads, smem, s, g3, (const uint32_t*)bits, (const uint32_t*)runs,
                        (const int32_t*)E, G, (const int32_t*)F, out, unsigned(ntiles), map);
         if (e != cudaSuccess) return e;
     }

@@ -81,6 +81,7 @@ struct Geom {
     int label_off;     // added to every label (row0 * W_total: labels are global)
     int force_top;     // the image's first row borders another strip
     int force_bottom;  // the image's last row borders another strip
+    int k3_early;      // K3 may read K1's outputs before its PDL wait (K1 finished before K3's predecessor)
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -97,6 +98,7 @@ struct __align__(16) Word {
 // the tile's edge-root list if its component touches a tile edge (its final
 // label then comes from the boundary analysis), else 0.
 constexpr int kRunCache = 256;  // run records K3 prefetches per tile
+constexpr int kRL = 32;         // last-row records K1 also copies to the end of a tile's record slot
 template <int TY>
 __host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
 // Edge-root list of a tile (written by K1): [0] = count n, [1..n] = image-local
@@ -259,7 +261,38 @@ __device__ __forceinline__ int ld_ca(const int32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ void red_min(int32_t* p, int v) {
+    asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+#ifndef CCL_K2_FULLC
+#define CCL_K2_FULLC 0
+#endif
 __device__ __forceinline__ int find_g(int32_t* G, int a) {
+#if CCL_K2_FULLC
+    // Walk to the root, then point every node of the walk straight at it with
+    // fire-and-forget atomic mins (no reply on the critical path).  A min can
+    // never undo a newer link (it only lowers an entry, and every value it
+    // writes is an ancestor in the node's set), so stale L1 reads cannot lose
+    // a union; chains that concurrent min-links string through the bands are
+    // cut for every later walker after the first.
+    int x = a, p = ld_ca(G + a);
+    CCL_LOOP_GUARD(fgc);
+    while (p != x) {
+        CCL_LOOP_TICK(fgc);
+        x = p;
+        p = ld_ca(G + x);
+    }
+    int y = a;
+    CCL_LOOP_GUARD(fgc2);
+    while (y > x) {
+        CCL_LOOP_TICK(fgc2);
+        const int next = ld_ca(G + y);
+        red_min(G + y, x);
+        y = next;
+    }
+    return x;
+#else
     int p = ld_ca(G + a);
     CCL_LOOP_GUARD(fgh);
 #ifdef CCL_STATS
@@ -282,6 +315,7 @@ __device__ __forceinline__ int find_g(int32_t* G, int a) {
     CCL_TASKSTAT(1, unsigned(hops));
 #endif
     return a;
+#endif
 }
 // (A two-pass full path compression here -- rewriting every visited node to
 // the root found through possibly stale L1 values -- lost unions under heavy
@@ -385,6 +419,21 @@ struct __align__(16) WordE {
 #ifndef CCL_K1_CAP16
 #define CCL_K1_CAP16 4576
 #endif
+#ifndef CCL_K1_UF2
+#define CCL_K1_UF2 0  // two-step local UF (up-link forest, then the remaining pairs)
+#endif
+#ifndef CCL_K1_V8
+#define CCL_K1_V8 1  // lane owns 32 contiguous pixels (256-bit loads), else 2 x 16 B + shuffles
+#endif
+#ifndef CCL_K1_RUNLOOP
+#define CCL_K1_RUNLOOP 0  // run lists: 0 two loops, 1 one joint loop, 2 peeled (<= 2 without a loop)
+#endif
+#ifndef CCL_K1_DENSE
+#define CCL_K1_DENSE (1 << 30)  // tiles with more runs take the random-priority local UF (r02: slower on noise, off)
+#endif
+#ifndef CCL_K1_UFDEDUP
+#define CCL_K1_UFDEDUP 0  // union each adjacency pair once (not from both of its runs)
+#endif
 #ifndef CCL_K1_BLOCKS
 #define CCL_K1_BLOCKS 5
 #endif
@@ -475,10 +524,37 @@ __device__ __forceinline__ void k1_union(int32_t* P, int a, int b) {
     union_r(P, a, b);
 }
 
+// Run-dense tiles (i.i.d. noise: ~4096 runs per 16-row tile, one giant
+// component): min-id linking strings the roots of a row into chains as long
+// as the row's run count (a zigzag between two rows links run j+1 under j for
+// every j at once), and the finds then walk them -- the union phase was 78 %
+// of a noise tile.  Here the unions link by a random priority instead (a
+// fixed bijective hash of the run id, ties impossible), which keeps expected
+// tree depth logarithmic; the component minimum (the canonical root, reading
+// R3) is then found with one atomic per run and every run is re-pointed at it,
+// so the flatten / edge / record steps see the same min-rooted forest as on
+// the sparse path.
+__device__ __forceinline__ uint32_t k1_prio(int x) {
+    return ((uint32_t(x) * 0x9E3779B1u) & 0xFFFF0000u) | uint32_t(x);  // hash high, id low: a total order
+}
+
+__device__ __forceinline__ void union_prio(int32_t* P, int a, int b) {
+    CCL_LOOP_GUARD(up);
+    while (true) {
+        CCL_LOOP_TICK(up);
+        a = find_r(P, a);
+        b = find_r(P, b);
+        if (a == b) return;
+        if (k1_prio(a) > k1_prio(b)) { const int t = a; a = b; b = t; }
+        if (atomicCAS(&P[a], a, b) == a) return;  // a stayed a root: linked under b
+    }
+}
+
 // Profiling builds only (DBG bit 2): per-tile phase timestamps.
 __device__ unsigned long long* g_k1_stamps = nullptr;
 __device__ unsigned long long* g_k3_stamps = nullptr;
 __device__ unsigned long long* g_k2_stamps = nullptr;  // per K2 task: start, end (globaltimer ns)
+__device__ unsigned long long* g_k2_phase = nullptr;   // per horizontal K2 task: masks in, records in, 1st batch done
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -493,27 +569,47 @@ __device__ __forceinline__ void k3_stamp(unsigned t, int k) {
 
 template <int TY>
 struct ImgRegs {
-    uint4 v[(TY + kWarps1 - 1) / kWarps1][2];
+    uint4 v[(TY + kWarps1 - 1) / kWarps1][2];  // row i of the warp: bytes 32*lane .. 32*lane + 31
 };
 
 template <int TY>
 __host__ __device__ constexpr bool k1_prefetches() { return TY <= 16; }
 
+// One lane's 32 contiguous pixels of a tile row: one 256-bit load when the
+// row is 32-byte aligned (W % 32 == 0 and an aligned image), else two 128-bit
+// loads (the row is 16-byte aligned on the vector path); pixels at or beyond
+// W read as background.  A warp instruction covers the whole 1024-px row.
+__device__ __forceinline__ void ld_px32(const uint8_t* p, int avail, bool v8, uint4& a, uint4& b) {
+    a = b = make_uint4(0, 0, 0, 0);
+    if (avail >= 32 && v8) {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
+    } else {
+        if (avail >= 16) a = ld_stream_u4(p);
+        if (avail >= 32) b = ld_stream_u4(p + 16);
+    }
+}
+
 template <int TY>
 __device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, unsigned t, int warp,
-                                            int lane, ImgRegs<TY>& pf) {
+                                            int lane, bool v8, ImgRegs<TY>& pf) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
 #pragma unroll
     for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
         const int y = (warp + i * kWarps1 < TY) ? id.y0 + warp + i * kWarps1 : g.H;
-        pf.v[i][0] = make_uint4(0, 0, 0, 0);
-        pf.v[i][1] = make_uint4(0, 0, 0, 0);
+        pf.v[i][0] = pf.v[i][1] = make_uint4(0, 0, 0, 0);
+#if CCL_K1_V8
+        const int x = id.x0 + 32 * lane;
+        if (y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, pf.v[i][0], pf.v[i][1]);
+#else
         if (y < g.H) {
             const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
             if (id.x0 + 16 * lane < g.W) pf.v[i][0] = ld_stream_u4(row + 16 * lane);
             if (id.x0 + 512 + 16 * lane < g.W) pf.v[i][1] = ld_stream_u4(row + 512 + 16 * lane);
         }
+#endif
     }
 }
 
@@ -543,7 +639,9 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
                                         int32_t* P, const Geom& g, unsigned t, const TileId& id, int v,
                                         int total, int32_t* G, uint32_t* R, int32_t* E, int warp, int lane) {
     const int tid = threadIdx.x;
-    // run lists: rs / re in raster order of the starts, P[k] = k
+    // run lists: rs / re in raster order of the starts (one loop over the
+    // word's starts and ends together: starts and ends alternate, so a word
+    // holds at most one more of either)
     {
         for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
             const int r = warp + i * kWarps1;
@@ -552,24 +650,75 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             const WordE w = sm.wd[r][lane];
             sm.wd[r][lane].pad = rb + w.pad;  // from here on: tile run id of the word's first start
             const int xb = lane << 5;
-            int k = rb + w.pad;
-            uint32_t bits_ = w.s;
-            while (bits_) {
-                const int bit = __ffs(bits_) - 1;
-                bits_ &= bits_ - 1;
-                rs[k] = uint16_t((xb + bit) | (r << 10));
-                P[k] = k;
-                ++k;
+            int ks = rb + w.pad;
+            int ke = ks - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
+            uint32_t sb = w.s, eb = w.e;
+#if CCL_K1_RUNLOOP == 2
+            // peeled: a word's first two starts / ends without a loop (97 % of
+            // texture words have <= 1 start); only denser words loop
+            {
+                const int cs = __popc(sb), ce = __popc(eb);
+                if (cs >= 1) rs[ks] = uint16_t((xb + __ffs(sb) - 1) | (r << 10));
+                sb &= sb - 1;
+                if (cs >= 2) rs[ks + 1] = uint16_t((xb + __ffs(sb) - 1) | (r << 10));
+                sb &= sb - 1;
+                if (ce >= 1) re[ke] = uint16_t(xb + __ffs(eb) - 1);
+                eb &= eb - 1;
+                if (ce >= 2) re[ke + 1] = uint16_t(xb + __ffs(eb) - 1);
+                eb &= eb - 1;
+                ks += 2;
+                ke += 2;
+                while (sb) {
+                    const int bit = __ffs(sb) - 1;
+                    sb &= sb - 1;
+                    rs[ks++] = uint16_t((xb + bit) | (r << 10));
+                }
+                while (eb) {
+                    const int bit = __ffs(eb) - 1;
+                    eb &= eb - 1;
+                    re[ke++] = uint16_t(xb + bit);
+                }
             }
-            k = rb + w.pad - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
-            bits_ = w.e;
-            while (bits_) {
-                const int bit = __ffs(bits_) - 1;
-                bits_ &= bits_ - 1;
-                re[k++] = uint16_t(xb + bit);
+#elif CCL_K1_RUNLOOP == 1
+            while (sb | eb) {
+                if (sb) {
+                    const int bit = __ffs(sb) - 1;
+                    sb &= sb - 1;
+                    rs[ks] = uint16_t((xb + bit) | (r << 10));
+#if !CCL_K1_UF2
+                    P[ks] = ks;
+#endif
+                    ++ks;
+                }
+                if (eb) {
+                    const int bit = __ffs(eb) - 1;
+                    eb &= eb - 1;
+                    re[ke++] = uint16_t(xb + bit);
+                }
             }
+#else
+            while (sb) {
+                const int bit = __ffs(sb) - 1;
+                sb &= sb - 1;
+                rs[ks] = uint16_t((xb + bit) | (r << 10));
+#if !CCL_K1_UF2
+                P[ks] = ks;
+#endif
+                ++ks;
+            }
+            while (eb) {
+                const int bit = __ffs(eb) - 1;
+                eb &= eb - 1;
+                re[ke++] = uint16_t(xb + bit);
+            }
+#endif
         }
         if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
+#if CCL_K1_RUNLOOP == 2 && !CCL_K1_UF2
+        // P[k] = k for every run, four entries per 128-bit store
+        for (int k = 4 * tid; k < total; k += 4 * kThreads1)
+            *reinterpret_cast<int4*>(P + k) = make_int4(k, k + 1, k + 2, k + 3);
+#endif
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
@@ -584,6 +733,94 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     // right of k's start, so it cannot reach k-1.  Each run therefore does at
     // most two unions, found in O(1) from the masks: no fan-in serialisation.
     constexpr int D = CONN == 8 ? 1 : 0;
+#if CCL_K1_UF2
+    // Two steps, every adjacency pair exactly once:
+    //  U1  P[k] = k's first upper neighbour (or k): a forest of up-links made
+    //      with plain stores -- each tree's root is its minimum run id (all
+    //      its other runs lie in lower rows) and no two threads touch one
+    //      entry, so no atomics and no retries;
+    //  U2  the remaining pairs (first lower neighbour jd of k, k) for which k
+    //      is NOT jd's first upper neighbour (i.e. run k-1 of the same row
+    //      also touches jd) are min-root unions on that forest.
+    // (Concurrent unions of all pairs at once built up-chains through every
+    // row and retried under contention: K1's union phase was 34 % of a
+    // texture tile and 78 % of a noise tile.)
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        int parent = k;
+        if (r > 0) {
+            const WordE uu = sm.wd[r - 1][p >> 5];
+            const uint32_t below = (1u << (p & 31)) - 1u;
+            const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
+            const int rsu = rs[ju];
+            if ((rsu >> 10) == r - 1 && (rsu & 1023) <= q) parent = ju;
+        }
+        if (DBG & 8) parent = k;
+        P[k] = parent;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = tid; k < total; k += kThreads1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        if (r + 1 >= TY || k == 0) continue;
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        const WordE ud = sm.wd[r + 1][p >> 5];
+        const uint32_t below = (1u << (p & 31)) - 1u;
+        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
+        const int rsd = rs[jd], rsp = rs[k - 1], ep = re[k - 1];
+        // jd touches k, and run k-1 (same row) touches jd too: k is a 2nd+ upper neighbour of jd
+        if ((rsd >> 10) == r + 1 && (rsd & 1023) <= q && (rsp >> 10) == r && ep + D >= (rsd & 1023))
+            k1_union<DBG>(P, jd, k);
+    }
+#else
+    if (total > CCL_K1_DENSE) {
+#pragma unroll 1
+        for (int k = tid; k < total; k += kThreads1) {
+            const int rsk = rs[k];
+            const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+            const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+            const WordE uu = sm.wd[r > 0 ? r - 1 : 0][p >> 5];
+            const WordE ud = sm.wd[r + 1 < TY ? r + 1 : TY - 1][p >> 5];
+            const uint32_t below = (1u << (p & 31)) - 1u;
+            const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
+            const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
+            const int rsu = rs[ju], rsd = rs[jd];
+            if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) union_prio(P, k, ju);
+            if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) union_prio(P, jd, k);
+        }
+        __syncthreads();
+        // component minimum at the root: high 16 bits = 0xFFFF - min member
+        // (unsigned atomicMax; the low 16 bits of a root entry stay its id);
+        // every other run is pointed straight at its root
+#pragma unroll 1
+        for (int k = tid; k < total; k += kThreads1) {
+            const int r = find_r_ro(P, k);
+            if (r != k) P[k] = r;
+            atomicMax(reinterpret_cast<unsigned*>(P + r), ((0xFFFFu - uint32_t(k)) << 16) | uint32_t(r));
+        }
+        __syncthreads();
+        // each root r hands its component to the minimum m: P[r] = m, P[m] = m
+#pragma unroll 1
+        for (int k = tid; k < total; k += kThreads1) {
+            const uint32_t v = uint32_t(P[k]);
+            if (v >> 16) {  // a root (only roots carry the packed minimum; P[m] = m below clears it)
+                const int m = int(0xFFFFu - (v >> 16));
+                P[k] = m;
+                if (m != k) P[m] = m;
+            }
+        }
+        __syncthreads();
+        // every run one hop further: its root's entry now names the minimum
+#pragma unroll 1
+        for (int k = tid; k < total; k += kThreads1) {
+            const int pk = P[k];
+            if (pk != k) P[k] = P[pk];
+        }
+    } else {
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int rsk = rs[k];
@@ -597,9 +834,21 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
         const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
         const int rsu = rs[ju], rsd = rs[jd];  // may be another row's run or the sentinel
+#if CCL_K1_UFDEDUP
+        // (jd, k) is also jd's own (jd, first upper neighbour) pair unless run
+        // k-1 of this row touches jd as well: union each pair once
+        const int rsp = k > 0 ? rs[k - 1] : 0, ep = k > 0 ? re[k - 1] : 0;
+        if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
+        if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q && k > 0 && (rsp >> 10) == r &&
+            ep + D >= (rsd & 1023))
+            k1_union<DBG>(P, jd, k);
+#else
         if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
         if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) k1_union<DBG>(P, jd, k);
+#endif
     }
+    }
+#endif
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
     // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
@@ -668,11 +917,18 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     if (tid < TY) st_keep(Eh + kEdgeLC + tid, sm.lc[tid]);
     else if (tid < 2 * TY) st_keep(Eh + kEdgeRC + tid - TY, sm.rc[tid - TY]);
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+    // the last row's first kRL records are also copied to the end of the
+    // tile's record slot (a fixed offset: the boundary analysis loads them in
+    // its first round trip) unless the tile's records reach that far
+    const int rb_last = sm.rbase[last_row];
+    const bool rl_copy = total <= runs_per_tile_cap<TY>() - kRL;
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int root = P[k] & 0xFFFF;
         const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
-        st_keep(Rt + k, uint32_t(rs[root]) | (uint32_t(tag) << 16));
+        const uint32_t rec = uint32_t(rs[root]) | (uint32_t(tag) << 16);
+        st_keep(Rt + k, rec);
+        if (rl_copy && k >= rb_last && k < rb_last + kRL) st_keep(Rt + runs_per_tile_cap<TY>() - kRL + (k - rb_last), rec);
     }
     __syncthreads();  // smem is reused by the next tile
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
@@ -681,7 +937,8 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
                                         ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
-                                        int32_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane) {
+                                        int32_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane,
+                                        bool v8) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
@@ -698,6 +955,15 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
         uint32_t m = 0;
         if (VEC) {
             uint4 v0 = cur.v[i][0], v1 = cur.v[i][1];
+#if CCL_K1_V8
+            if (!k1_prefetches<TY>()) {  // tall tiles: load in place (register budget)
+                v0 = v1 = make_uint4(0, 0, 0, 0);
+                const int x = id.x0 + 32 * lane;
+                if (y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, v0, v1);
+            }
+            // the lane's own 32 contiguous pixels: no cross-lane assembly
+            m = nz16(v0) | (nz16(v1) << 16);
+#else
             if (!k1_prefetches<TY>()) {  // tall tiles: load in place (register budget)
                 v0 = v1 = make_uint4(0, 0, 0, 0);
                 if (y < g.H) {
@@ -706,11 +972,13 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
                     if (id.x0 + 512 + 16 * lane < g.W) v1 = ld_stream_u4(row + 512 + 16 * lane);
                 }
             }
+            // lane l holds pixels 16l.. and 512+16l..: assemble word l by shuffles
             const uint32_t h0 = nz16(v0), h1 = nz16(v1);
             const int src = (2 * lane) & 31;
             const uint32_t a0 = __shfl_sync(kFull, h0, src), a1 = __shfl_sync(kFull, h0, src + 1);
             const uint32_t b0 = __shfl_sync(kFull, h1, src), b1 = __shfl_sync(kFull, h1, src + 1);
             m = lane < 16 ? (a0 | (a1 << 16)) : (b0 | (b1 << 16));
+#endif
         } else {
             const uint8_t* row = im + size_t(y < g.H ? y : 0) * size_t(g.W);
 #pragma unroll 4
@@ -727,7 +995,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     }
     // the pixels are in the masks now: the same registers receive the block's
     // next tile, in flight during the rest of this one
-    if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, cur);
+    if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, v8, cur);
     // tall tiles (no register room for a second tile): the next tile's rows
     // are pulled into L2 with bulk prefetches instead, one per row
     if (VEC && !k1_prefetches<TY>() && tnext < ntiles && warp == kWarps1 - 1 && lane < TY) {
@@ -845,6 +1113,10 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     s_w[0][lane] = Word{cur, sc, 0, ic - __popc(sc)};
     s_w[1][lane] = Word{up, su, 0, iu - __popc(su)};
     __syncwarp();
+#ifdef CCL_K2_PHASES  // profiling harness only (tools/k1_phases.cu)
+    const unsigned ptask = blockIdx.x * 8u + (threadIdx.x >> 5);
+    if (g_k2_phase && lane == 0) g_k2_phase[4 * size_t(ptask)] = gtimer();
+#endif
     const uint32_t o = cur & up, oL = curL & upL;
     uint32_t ev = o & ~((o << 1) | (oL >> 31));
     uint32_t ne = 0, nw = 0;
@@ -936,10 +1208,17 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
             }
         }
         __syncwarp();
+#ifdef CCL_K2_PHASES
+        if (g_k2_phase && lane == 0 && g_k2_phase[4 * size_t(ptask) + 1] == 0) g_k2_phase[4 * size_t(ptask) + 1] = gtimer();
+#endif
         for (int base = 0; base < total; base += 32) {
             const int i = base + lane;
             const int2 pr = i < total ? pairs[i] : make_int2(-1, -1);
             warp_union_pairs<NOUNION>(Gb, pr.x, pr.y, last);
+#ifdef CCL_K2_PHASES
+            __syncwarp();
+            if (g_k2_phase && lane == 0 && g_k2_phase[4 * size_t(ptask) + 2] == 0) g_k2_phase[4 * size_t(ptask) + 2] = gtimer();
+#endif
         }
         __syncwarp();
     }
@@ -1041,10 +1320,12 @@ __global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const 
     constexpr bool PF = VEC && k1_prefetches<TY>();
     // one register set: loaded with tile t before the loop, then refilled with
     // the block's next tile as soon as the current one is in the masks
+    // 256-bit image loads need 32-byte aligned rows
+    const bool v8 = ((g.W & 31) == 0) && ((reinterpret_cast<uintptr_t>(img) & 31) == 0);
     ImgRegs<TY> a;
-    if (PF) k1_prefetch<TY>(img, g, t, warp, lane, a);
+    if (PF) k1_prefetch<TY>(img, g, t, warp, lane, v8, a);
     while (t < ntiles) {
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, k1x, warp, lane);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, k1x, warp, lane, v8);
         t += gridDim.x;
     }
 }
@@ -1344,6 +1625,8 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
     {
         const int total = __shfl_sync(kFull, v, TY - 1);
         for (int i = tid; i < (total + 31) / 32; i += kThreads) l2_discard(Rt + 32 * i);
+        if (tid == kThreads - 1 && total <= runs_per_tile_cap<TY>() - kRL)
+            l2_discard(Rt + runs_per_tile_cap<TY>() - kRL);  // the last-row copy (K2's fixed-offset slot)
         if ((W & 1023) == 0 && lane < TY / kWarps) {
             const int y = y0 + warp + lane * kWarps;
             if (y < g.H)
@@ -1437,9 +1720,22 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
         sm.consumed = 0;
     }
     __syncthreads();
-    pdl_wait();
     unsigned t = blockIdx.x;
     if (t >= ntiles) return;
+    // The mask words and run records are K1's outputs, complete before the
+    // boundary analysis started: the compute warps load their first two tiles'
+    // share BEFORE waiting for the boundary analysis to finish (under PDL this
+    // block is already resident while it drains).
+    LinkRegs<TY> a, b;
+    if (warp < kWarps && g.k3_early) {
+        k3_prefetch<TY>(bits, R, g, t, warp, lane, a);
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
+    }
+    pdl_wait();
+    if (warp < kWarps && !g.k3_early) {  // K3 right after K1 (no boundaries): K1's outputs only after the wait
+        k3_prefetch<TY>(bits, R, g, t, warp, lane, a);
+        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
+    }
     // The block's first tile: all 9 warps resolve its edge roots together
     // (one chain latency instead of n / 32 of them on the helper alone -- the
     // compute warps would otherwise wait for it); the helper takes the rest.
@@ -1454,11 +1750,9 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
         k3_helper<TY, RES>(sm, g, E, G, F, ntiles, j0);
         return;
     }
-    LinkRegs<TY> a, b;
-    k3_prefetch<TY>(bits, R, g, t, warp, lane, a);
     int j = 0;
     while (true) {
-        if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
+        if (j > 0 && t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
         k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, j++, a, R, out, &tmap, warp, lane);
         t += gridDim.x;
         if (t >= ntiles) break;

@@ -138,6 +138,37 @@ __global__ void w_bulk(int32_t* p, size_t nchunks) {
     }
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// K3's store pattern without its compute: persistent blocks of 8 warps walk
+// 1024 x 16 int32 tiles (t = block, block + grid, ...); each warp stores its
+// two 4 KB rows of a tile with bulk S2G copies from its own smem row buffer
+// (waiting for the previous store to have read the buffer first).
+template <int ROWS_PER_STORE>
+__global__ void w_k3pattern(int32_t* out, int H, int W, unsigned ntiles) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int4* buf = reinterpret_cast<int4*>(sm + warp * 4096 * ROWS_PER_STORE);
+    const int tiles_x = W / 1024;
+    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tx = t % tiles_x, ty = t / tiles_x;
+        for (int r = warp * ROWS_PER_STORE; r < 16; r += 8 * ROWS_PER_STORE) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            for (int q = lane; q < 256 * ROWS_PER_STORE; q += 32) buf[q] = make_int4(int(t), r, q, 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                for (int rr = 0; rr < ROWS_PER_STORE; ++rr) {
+                    int32_t* dst = out + size_t(ty * 16 + r + rr) * W + tx * 1024;
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(unsigned(__cvta_generic_to_shared(buf + 256 * rr))), "r"(4096u)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void copy_v4(const uint4* a, uint4* b, size_t n) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         b[i] = a[i];
@@ -231,6 +262,21 @@ int main() {
                 snprintf(nm, sizeof nm, "write bulk 16KB x4, %d blk/SM", per);
                 rep(nm, timeit([&] { k3<<<sms * per, 256, 4 * 16384>>>(out, nw / 16384); }), nw);
             }
+        }
+    }
+    {
+        const int H = 8192, W = 8192;
+        const unsigned ntiles = (H / 16) * (W / 1024);
+        auto k1 = w_k3pattern<1>;
+        auto k2 = w_k3pattern<2>;
+        CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096));
+        CK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192));
+        for (int per : {3, 4, 6}) {
+            char nm[80];
+            snprintf(nm, sizeof nm, "write K3 pattern 4KB rows, %d blk/SM", per);
+            rep(nm, timeit([&] { k1<<<sms * per, 256, 8 * 4096>>>(out, H, W, ntiles); }), nw);
+            snprintf(nm, sizeof nm, "write K3 pattern 2x4KB per store, %d blk/SM", per);
+            rep(nm, timeit([&] { k2<<<sms * per, 256, 8 * 8192>>>(out, H, W, ntiles); }), nw);
         }
     }
     rep("copy v4 (256 MiB -> 256 MiB, r+w bytes)", timeit([&] {

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <vector>
 
+#define CCL_K2_PHASES 1
 #include "../paper_1708_08180_b200/csrc/ccl_kernels.cuh"
 #include <cudaTypedefs.h>
 static void* g_k1x = nullptr;  // K1 overflow scratch
@@ -34,6 +35,24 @@ __global__ void read_floor(const uint4* p, size_t n, unsigned* sink) {
 __global__ void write_floor(int32_t* p, size_t n4) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x)
         ccl::st_stream_i4(p + 4 * i, int(i), 0, 1, 2);
+}
+
+// Touch K1's outputs (mask, the used part of every tile's run records, edge
+// blocks, the edge roots' parent sectors) so they are L2-resident: isolates
+// how much of K2's time is DRAM latency on K1's outputs.
+__global__ void touch_k1_outputs(const uint32_t* bits, size_t nwords, const uint32_t* R, int rcap,
+                                 const int32_t* E, const int32_t* G, unsigned ntiles, unsigned* sink) {
+    unsigned acc = 0;
+    const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x, nt = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = tid; i < nwords; i += nt) acc ^= __ldcg(bits + i);
+    for (size_t i = tid; i < size_t(ntiles) * 512; i += nt) acc ^= __ldcg(R + (i / 512) * rcap + (i % 512));
+    for (size_t t = tid; t < ntiles; t += nt) {
+        const int32_t* Et = E + t * ccl::kEdgeCap;
+        const int n = __ldcg(Et);
+        for (int j = 0; j < ccl::kEdgeList + n && j < ccl::kEdgeCap; ++j) acc ^= __ldcg(Et + j);
+        for (int j = 0; j < n; ++j) acc ^= __ldcg(G + __ldcg(Et + ccl::kEdgeList + j));
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
 }
 
 template <typename F>
@@ -107,7 +126,10 @@ int main(int argc, char** argv) {
     float w = timeit([&] { write_floor<<<sms * 8, 256>>>(out, n / 4); }, flush, fb);
     printf("%-34s %8.1f us  %7.1f GB/s\n", "write floor (labels, 4 B/px)", w, 4 * n / w / 1e3);
 
-    constexpr int TY = 16;
+#ifndef KP_TY
+#define KP_TY 16
+#endif
+    constexpr int TY = KP_TY;
     ccl::Geom g;
     g.B = 1;
     g.H = H;
@@ -124,6 +146,7 @@ int main(int argc, char** argv) {
     g.div_tx1 = ccl::FastDiv(std::max(1, g.tiles_x - 1));
     g.div_vg = ccl::FastDiv((g.tiles_y + 32 / TY - 1) / (32 / TY));
     g.label_off = g.force_top = g.force_bottom = 0;
+    g.k3_early = 1;
     for (int per_sm : {4, 5}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
@@ -183,10 +206,33 @@ int main(int argc, char** argv) {
         printf("%-34s %8.1f us\n", nm, 1000.f * tot2 / 20);
     };
     time_k2(ccl::k_boundary<TY, 8, 0>, "K2 full");
+    CK(cudaFuncSetAttribute(ccl::k_boundary<TY, 8, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 40));
+    time_k2(ccl::k_boundary<TY, 8, 0>, "K2 full (carveout 40)");
+
     time_k2(ccl::k_boundary<TY, 8, 1>, "K2 horizontal only");
     time_k2(ccl::k_boundary<TY, 8, 2>, "K2 vertical only");
     time_k2(ccl::k_boundary<TY, 8, 3>, "K2 empty (launch)");
     time_k2(ccl::k_boundary<TY, 8, 5>, "K2 horizontal, no unions");
+    {
+        // K2 with K1's outputs pulled into L2 first (touch kernel outside the events)
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        float tot2 = 0;
+        for (int i = 0; i < 23; ++i) {
+            CK(cudaMemsetAsync(flush, i, fb));
+            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            touch_k1_outputs<<<sms * 4, 256>>>(bits, g.nwords, R, ccl::runs_per_tile_cap<TY>(), E, G, ntiles, sink);
+            CK(cudaEventRecord(a));
+            ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            if (i >= 3) tot2 += ms;
+        }
+        printf("%-34s %8.1f us\n", "K2 full, K1 outputs L2-resident", 1000.f * tot2 / 20);
+    }
     {
         // per-task K2 timeline (globaltimer): where does the kernel's time go?
         const long long nt = n_h + n_v;
@@ -194,9 +240,35 @@ int main(int argc, char** argv) {
         CK(cudaMalloc(&st2, size_t(nt) * 16));
         CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &st2, sizeof(st2)));
         CK(cudaMemsetAsync(flush, 1, fb));
+        unsigned long long* ph;
+        CK(cudaMalloc(&ph, size_t(nt) * 32));
+        for (int ver = 0; ver < 1; ++ver) {
+        CK(cudaMemset(ph, 0, size_t(nt) * 32));
+        if (ver == 0) CK(cudaMemcpyToSymbol(ccl::g_k2_phase, &ph, sizeof(ph)));
         k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
-        ccl::k_boundary<TY, 8, 8><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
+        auto kt = ccl::k_boundary<TY, 8, 8>;
+        kt<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
         CK(cudaDeviceSynchronize());
+        printf("[%s] ", ver == 0 ? "K2" : "K2v2");
+        if (ver == 0) {
+            unsigned long long* z = nullptr;
+            CK(cudaMemcpyToSymbol(ccl::g_k2_phase, &z, sizeof(z)));
+            std::vector<unsigned long long> hp(size_t(nt) * 4), hs0(size_t(nt) * 2);
+            CK(cudaMemcpy(hp.data(), ph, hp.size() * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(hs0.data(), st2, hs0.size() * 8, cudaMemcpyDeviceToHost));
+            std::vector<double> d0, d1, d2, d3;
+            for (long long i = 0; i < n_h; ++i) {
+                if (!hp[4 * i] || !hp[4 * i + 1] || !hp[4 * i + 2]) continue;
+                d0.push_back((hp[4 * i] - hs0[2 * i]) / 1000.0);
+                d1.push_back((hp[4 * i + 1] - hp[4 * i]) / 1000.0);
+                d2.push_back((hp[4 * i + 2] - hp[4 * i + 1]) / 1000.0);
+                d3.push_back((hs0[2 * i + 1] - hp[4 * i + 2]) / 1000.0);
+            }
+            auto pc = [](std::vector<double> v, double q) { std::sort(v.begin(), v.end()); return v.empty() ? 0.0 : v[size_t(q * (v.size() - 1))]; };
+            printf("K2 horizontal phases (us, p50/p90/max): masks-in %.2f/%.2f/%.2f  records-in %.2f/%.2f/%.2f  1st batch %.2f/%.2f/%.2f  rest %.2f/%.2f/%.2f  (n=%zu)\n",
+                   pc(d0, .5), pc(d0, .9), pc(d0, 1), pc(d1, .5), pc(d1, .9), pc(d1, 1), pc(d2, .5), pc(d2, .9), pc(d2, 1),
+                   pc(d3, .5), pc(d3, .9), pc(d3, 1), d0.size());
+        }
         std::vector<unsigned long long> hs(size_t(nt) * 2);
         CK(cudaMemcpy(hs.data(), st2, hs.size() * 8, cudaMemcpyDeviceToHost));
         unsigned long long t0 = ~0ull, t1 = 0;
@@ -215,6 +287,7 @@ int main(int argc, char** argv) {
                    kind ? "vertical  " : "horizontal", pct(d, .5), pct(d, .9), pct(d, .99), pct(d, 1.0), pct(st, .5),
                    pct(st, 1.0), pct(en, .5), pct(en, .99), pct(en, 1.0));
         }
+        }
 #ifdef CCL_STATS
         {   // the slowest tasks: what do they do?
             unsigned* ts;
@@ -228,16 +301,14 @@ int main(int argc, char** argv) {
             CK(cudaMemcpy(hts.data(), ts, hts.size() * 4, cudaMemcpyDeviceToHost));
             std::vector<long long> idx(nt);
             for (long long i = 0; i < nt; ++i) idx[i] = i;
-            std::sort(idx.begin(), idx.end(), [&](long long x, long long y) {
-                return hs[2 * x + 1] - hs[2 * x] > hs[2 * y + 1] - hs[2 * y];
-            });
+            std::sort(idx.begin(), idx.end(), [&](long long x, long long y) { return hts[4 * x] > hts[4 * y]; });
             double sst = 0, sho = 0, sre = 0, sro = 0;
             for (long long i = 0; i < nt; ++i) { sst += hts[4*i]; sho += hts[4*i+1]; sre += hts[4*i+2]; sro += hts[4*i+3]; }
             printf("K2 per task mean: steps %.1f hops %.1f retries %.2f rounds %.2f\n", sst / nt, sho / nt, sre / nt, sro / nt);
             for (int k = 0; k < 12 && k < nt; ++k) {
                 const long long i = idx[k];
-                printf("  slow task %lld (%s): %.2f us  steps %u hops %u retries %u rounds %u\n", i, i < n_h ? "h" : "v",
-                       (hs[2 * i + 1] - hs[2 * i]) / 1000.0, hts[4*i], hts[4*i+1], hts[4*i+2], hts[4*i+3]);
+                printf("  busiest task %lld (%s): steps %u hops %u retries %u rounds %u\n", i, i < n_h ? "h" : "v",
+                       hts[4*i], hts[4*i+1], hts[4*i+2], hts[4*i+3]);
             }
             unsigned* np2 = nullptr;
             CK(cudaMemcpyToSymbol(ccl::g_k2_taskstat, &np2, sizeof(np2)));
@@ -311,6 +382,10 @@ int main(int argc, char** argv) {
     }
     CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     CK(cudaFuncSetAttribute(k3s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+    for (int grid3 : {370, 390, 410, 428, 444}) {
+        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
+        printf("K3 grid %4d (%.2f tiles/block)     %8.1f us\n", grid3, double(ntiles) / grid3, us);
+    }
     for (int per_sm : {3, 4, 5}) {
         const int grid3 = std::min<int>(ntiles, sms * per_sm);
         float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
