@@ -28,8 +28,8 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, k1x_bytes;
-    size_t total() const { return G_bytes + bits_bytes + runs_bytes + 2 * edge_bytes + k1x_bytes; }
+    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, k1x_bytes;
+    size_t total() const { return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + k1x_bytes; }
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -74,20 +74,28 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.force_top = 0;
     p.g.force_bottom = 0;
     p.g.k3_early = 1;
-    p.G_bytes = align_up(size_t(B) * size_t(H) * size_t(W) * sizeof(int32_t));
+    p.g.ntiles = unsigned(int64_t(B) * p.g.tiles_x * p.g.tiles_y);
+    // edge slots (the boundary analysis' union-find nodes, 8 B each) and their
+    // resolved labels in strip mode (4 B each): edge_slots(TY) per tile, sized
+    // for the tile configuration that needs the most (ccl_kernels.cuh)
+    const size_t tiles8 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 7) / 8);
+    const size_t tiles16 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 15) / 16);
+    const size_t tiles32 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 31) / 32);
+    const size_t slots = std::max({tiles8 * ccl::edge_slots(8), tiles16 * ccl::edge_slots(16),
+                                   tiles32 * ccl::edge_slots(32)});
+    if (slots >= size_t(INT32_MAX)) return CCL_ERR_TOO_LARGE;
+    p.G_bytes = align_up(slots * sizeof(uint64_t));
+    p.F_bytes = align_up(slots * sizeof(int32_t));
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
     // per-run records: capacity of the worst case (alternating pixels) for the
     // tallest tile config, so the size does not depend on tile_rows
     const size_t rows32 = size_t((H + 31) / 32) * 32;
     p.runs_bytes = align_up(size_t(B) * size_t(p.g.tiles_x) * rows32 * (ccl::kTileW / 2) * sizeof(uint32_t));
-    // edge-root lists E and resolved labels F: kEdgeCap ints per tile, sized
-    // for the most tiles any config makes (tile_rows = 8)
-    const size_t tiles8 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 7) / 8);
+    // edge briefs E: kEdgeCap ints per tile, for the most tiles any config
+    // makes (tile_rows = 8)
     p.edge_bytes = align_up(tiles8 * ccl::kEdgeCap * sizeof(int32_t));
     // K1 scratch slots for tiles over the shared-memory run capacity (one per
     // K1 block; tile_rows = 8 never overflows), sized for the larger need
-    const size_t tiles16 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 15) / 16);
-    const size_t tiles32 = size_t(B) * size_t(p.g.tiles_x) * size_t((H + 31) / 32);
     p.k1x_bytes = align_up(std::max(std::min(tiles16, size_t(ccl::k1x_slots<16>())) * ccl::k1x_slot_bytes<16>(),
                                     std::min(tiles32, size_t(ccl::k1x_slots<32>())) * ccl::k1x_slot_bytes<32>()));
     return CCL_OK;
@@ -255,7 +263,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     cudaError_t e = setup_attrs<TY, CONN, VEC>();
     if (e != cudaSuccess) return e;
     const ccl::Geom& g = p.g;
-    int32_t* G = static_cast<int32_t*>(ws);
+    uint64_t* G = static_cast<uint64_t*>(ws);
     uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes);
     uint32_t* runs = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes);
     int32_t* E = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes + p.runs_bytes);
@@ -266,7 +274,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     // persistent K1/K3: one wave of resident blocks walks all tiles
     const unsigned grid1 = unsigned(std::min<long long>(
         std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)), ccl::k1x_slots<TY>()));
-    void* k1x = reinterpret_cast<char*>(F) + p.edge_bytes;
+    void* k1x = reinterpret_cast<char*>(F) + p.F_bytes;
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
         ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads1, smem_bytes_k1<TY>(), s>>>(

@@ -82,6 +82,7 @@ struct Geom {
     int force_top;     // the image's first row borders another strip
     int force_bottom;  // the image's last row borders another strip
     int k3_early;      // K3 may read K1's outputs before its PDL wait (K1 finished before K3's predecessor)
+    unsigned ntiles;   // tiles of the whole batch: the stride of the edge-slot numbering
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -98,24 +99,39 @@ struct __align__(16) Word {
 // the tile's edge-root list if its component touches a tile edge (its final
 // label then comes from the boundary analysis), else 0.
 constexpr int kRunCache = 256;  // run records K3 prefetches per tile
-constexpr int kRL = 32;         // last-row records K1 also copies to the end of a tile's record slot
+constexpr int kRL = 32;         // run records of each boundary row K1 copies into the edge brief
 template <int TY>
 __host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
-// Edge-root list of a tile (written by K1): [0] = count n, [1..n] = image-local
-// raster index of each edge-touching local root, in run order.  The resolved
-// final labels (written by the boundary analysis) live at the same offsets - 1
-// of a parallel array F.  Capacity: <= 512 runs per tile row x 2 rows + 2 TY
-// column pixels; 1120 covers TY <= 32.
-// Per-tile edge block E[t] (kEdgeCap ints), written by K1:
-//   [0] n = number of edge-touching local roots; [1] run id of the first run of
-//   the tile's last row; [kEdgeLC + r] / [kEdgeRC + r] = image-local raster
-//   index of the local root of pixel (r, 0) / (r, 1023), or -1 (background or
-//   no neighbouring tile); [kEdgeList + i], i < n = the edge roots, in run order.
+// Edge slots (the boundary analysis' union-find nodes): the i-th edge-touching
+// local root of tile t (i < its edge count n) is slot i * ntiles + t -- slot
+// numbers are "edge index major", so the few slots a natural image uses per
+// tile (i < ~30) are packed into a few MB instead of being scattered over a
+// raster-indexed H*W array (K2's dependent loads cost ~4x when they touch
+// hundreds of 2 MB pages: profiles/r02_latency_sparse_pages.txt).  Slot s's
+// 64-bit entry G[s] = (X << 32) | parent slot, X = the parent's image-local
+// raster index (a root: its own), so the minimum-raster-index root policy
+// (reading R11) is an unsigned 64-bit atomicMin.
+// Within that order a 128-byte line holds 16 consecutive edge indices of ONE
+// tile (line q of tile t holds i = 16q .. 16q+15), so no two tiles' entries
+// share a line or sector (a layout with one tile per 8-byte step measured
+// K2 25 -> 37 us: atomics and pointer-jumping stores of different tiles on
+// one line), and K1 writes each tile's entries as whole 32-byte sectors.
+__host__ __device__ constexpr int edge_slots(int TY) { return (2 * (kTileW / 2) + 2 * TY + 15) / 16 * 16; }
+__host__ __device__ inline unsigned edge_slot(unsigned ntiles, int i, unsigned t) {
+    return ((unsigned(i) >> 4) * ntiles + t) * 16u + (unsigned(i) & 15u);
+}
+
+// Per-tile edge brief E[t] (kEdgeCap ints), written by K1:
+//   [0] n = number of edge-touching local roots; [1] run id of the first run
+//   of the tile's last row; [kEdgeLC + r] / [kEdgeRC + r] = slot of the local
+//   root of pixel (r, 0) / (r, 1023), or -1; [kEdgeR0 + i] / [kEdgeRL + i], i
+//   < 32 = the run records of the first 32 runs of the first / last row (the
+//   boundary analysis reads them in its first round trip).
 constexpr int kEdgeLC = 2;
 constexpr int kEdgeRC = 34;
-constexpr int kEdgeList = 66;
-constexpr int kEdgeCap = 1152;
-constexpr int kEdgeCache = 32;  // resolved labels K3 prefetches per tile
+constexpr int kEdgeR0 = 66;
+constexpr int kEdgeRL = 98;
+constexpr int kEdgeCap = 136;
 
 // ------------------------------------------------------------------ helpers
 // 4-bit mask of the nonzero bytes of w: the carry trick puts byte i's "nonzero"
@@ -183,6 +199,13 @@ __device__ __forceinline__ void st_keep(T* p, T v) {
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(*reinterpret_cast<uint32_t*>(&v)),
                  "l"(l2_keep_policy())
                  : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void st_keep_u64(uint64_t* p, uint64_t v) {
+#if CCL_K1_KEEP
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(l2_keep_policy()) : "memory");
 #else
     *p = v;
 #endif
@@ -637,7 +660,7 @@ __device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uin
 template <int TY, int CONN, int DBG>
 __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ rs, uint16_t* __restrict__ re,
                                         int32_t* P, const Geom& g, unsigned t, const TileId& id, int v,
-                                        int total, int32_t* G, uint32_t* R, int32_t* E, int warp, int lane) {
+                                        int total, uint64_t* G, uint32_t* R, int32_t* E, int warp, int lane) {
     const int tid = threadIdx.x;
     // run lists: rs / re in raster order of the starts (one loop over the
     // word's starts and ends together: starts and ends alternate, so a word
@@ -854,13 +877,10 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
     // index conversion): every run points at its root; the first run to find
     // that its root's component touches a tile edge (top / bottom row run,
-    // left / right column pixel) claims the root (bit 31), appends it to the
-    // tile's edge-root list, writes its global parent entry and tags the root
-    // with 1 + its list index (list order = claim order: any bijection works,
-    // the labels do not depend on it).  The global parent entries G[r] = r
-    // are written as whole 32-byte sectors (identity for the 8 pixels: no
-    // other entry of G is ever read) so the boundary analysis' atomics and
-    // loads hit fully valid L2 sectors instead of filling from DRAM.
+    // left / right column pixel) claims the root (bit 31), takes the next
+    // edge index i of the tile and tags the root with 1 + i (claim order: any
+    // bijection works, the labels do not depend on it); the root becomes
+    // edge slot i * ntiles + t with entry (global raster index << 32) | slot.
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
     const int W = g.W, x0 = id.x0, y0 = id.y0;
     // rows that border another tile (or, in strip mode, another strip)
@@ -868,9 +888,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     const bool top = y0 > 0 || g.force_top;
     const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
     const bool left = x0 > 0, right = x0 + kTileW < W;
-    int32_t* Gb = G + size_t(id.b) * size_t(g.npx);
     int32_t* Eh = E + size_t(t) * kEdgeCap;
-    int32_t* Et = Eh + kEdgeList;
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int root = find_r_ro(P, k);
@@ -880,26 +898,12 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         const bool hrow = (r == 0 && top) || (r == last_row && bottom);
         const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
         if (hrow || lc || rc) {
-            const int rr = rs[root];
-            const int gr = (y0 + (rr >> 10)) * W + x0 + (rr & 1023);
             if (!(atomicOr(&P[root], int(0x80000000u)) & int(0x80000000u))) {
                 const int idx = atomicAdd(&sm.ecount, 1);
                 P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
-                st_keep(Et + idx, gr);
-                if ((g.npx & 7) == 0) {
-                    // whole sector, identity: harmless for the 7 neighbours
-                    // (every root entry is still its own index during K1, all
-                    // other entries are never read); images are sector-aligned
-                    const int base = gr & ~7;
-                    int4* sec = reinterpret_cast<int4*>(Gb + base);
-                    st_keep_v4(sec, make_int4(base, base + 1, base + 2, base + 3));
-                    st_keep_v4(sec + 1, make_int4(base + 4, base + 5, base + 6, base + 7));
-                } else {
-                    st_keep(Gb + gr, gr);
-                }
             }
-            if (lc) sm.lc[r] = gr;
-            if (rc) sm.rc[r] = gr;
+            if (lc) sm.lc[r] = k;  // the column pixel's run (its root's slot after the claims)
+            if (rc) sm.rc[r] = k;
         }
     }
     if (DBG & 2) {
@@ -909,35 +913,67 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
-    // edge block header + column roots, and the per-run records for K3 / K2
+    // edge brief: header, column-root slots; per-run records for K3 / K2
     if (tid == 0) {
         st_keep(Eh, sm.ecount);
         st_keep(Eh + 1, sm.rbase[last_row]);  // first run of the last valid row
     }
-    if (tid < TY) st_keep(Eh + kEdgeLC + tid, sm.lc[tid]);
-    else if (tid < 2 * TY) st_keep(Eh + kEdgeRC + tid - TY, sm.rc[tid - TY]);
+    if (tid < 2 * TY) {
+        const int k = tid < TY ? sm.lc[tid] : sm.rc[tid - TY];
+        int slot = -1;
+        if (k >= 0) slot = int(edge_slot(g.ntiles, ((P[P[k] & 0xFFFF] >> 16) & 0x7FFF) - 1, t));
+        st_keep(Eh + (tid < TY ? kEdgeLC + tid : kEdgeRC + tid - TY), slot);
+    }
     uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
-    // the last row's first kRL records are also copied to the end of the
-    // tile's record slot (a fixed offset: the boundary analysis loads them in
-    // its first round trip) unless the tile's records reach that far
     const int rb_last = sm.rbase[last_row];
-    const bool rl_copy = total <= runs_per_tile_cap<TY>() - kRL;
+    const int ne = sm.ecount;  // (read before the last barrier: the next tile resets it)
 #pragma unroll 1
     for (int k = tid; k < total; k += kThreads1) {
         const int root = P[k] & 0xFFFF;
-        const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge-list index, or 0
+        const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge index, or 0
         const uint32_t rec = uint32_t(rs[root]) | (uint32_t(tag) << 16);
         st_keep(Rt + k, rec);
-        if (rl_copy && k >= rb_last && k < rb_last + kRL) st_keep(Rt + runs_per_tile_cap<TY>() - kRL + (k - rb_last), rec);
+        // the first kRL runs of the first and last rows again in the edge
+        // brief: the boundary analysis' first round trip
+        if (k < kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeR0 + k, rec);
+        if (k >= rb_last && k < rb_last + kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeRL + (k - rb_last), rec);
+        // edge index -> root run (re, the run ends, is free after the flatten)
+        if (root == k && tag) re[tag - 1] = uint16_t(k);
     }
-    __syncthreads();  // smem is reused by the next tile
+    __syncthreads();  // smem is reused by the next tile (rs / re / P are not rewritten
+                      // before its first barrier: the slot writes below still read them)
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
+    // the edge slots' initial entries (raster index << 32 | slot: every edge
+    // root its own set), four per thread = one whole 32-byte sector, so the
+    // boundary analysis' loads and atomics hit fully valid L2 sectors
+    {
+#pragma unroll 1
+        for (int j = tid; 4 * j < ne; j += kThreads1) {
+            uint32_t v[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = 4 * j + q;
+                uint32_t gr = 0, sl = 0;
+                if (i < ne) {
+                    const int rr = rs[re[i]];
+                    gr = uint32_t((y0 + (rr >> 10)) * W + x0 + (rr & 1023));
+                    sl = edge_slot(g.ntiles, i, t);
+                }
+                v[2 * q] = sl;
+                v[2 * q + 1] = gr;
+            }
+            int4* sec = reinterpret_cast<int4*>(G + edge_slot(g.ntiles, 4 * j, t));
+            st_keep_v4(sec, make_int4(int(v[0]), int(v[1]), int(v[2]), int(v[3])));
+            st_keep_v4(sec + 1, make_int4(int(v[4]), int(v[5]), int(v[6]), int(v[7])));
+        }
+    }
 }
+
 
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
                                         ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
-                                        int32_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane,
+                                        uint64_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane,
                                         bool v8) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
@@ -1042,19 +1078,98 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
 // the union walks over the roots' parent entries in G.
 // K1's outputs are read with ld.global.cg (L2).
 
+// ---------------------------------------------- edge-slot union-find (K2)
+// G[s] = (X << 32) | parent slot, X = the parent's raster index (a root: its
+// own).  Same protocol as the 32-bit raster-indexed form it replaces (reading
+// R11: lock-free minimum-root union, retry from the displaced parent, path
+// halving that only ever stores an ancestor's entry), with the order "smaller
+// raster index" carried in the high word so one 64-bit atomicMin links.
+__device__ __forceinline__ uint64_t ld_ca64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_volatile64(uint64_t* p, uint64_t v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Root entry of slot a's set (path halving: a re-pointed at its grandparent).
+__device__ __forceinline__ uint64_t find_e(uint64_t* G, unsigned a) {
+    uint64_t v = ld_ca64(G + a);
+    CCL_LOOP_GUARD(fe);
+#ifdef CCL_STATS
+    unsigned long long hops = 0;
+    atomicAdd(&g_stat_finds, 1ull);
+#endif
+    while (unsigned(v) != a) {
+        CCL_LOOP_TICK(fe);
+#ifdef CCL_STATS
+        ++hops;
+#endif
+        const unsigned p = unsigned(v);
+        const uint64_t w = ld_ca64(G + p);  // p's entry: its parent (the grandparent)
+        if (unsigned(w) != p) st_volatile64(G + a, w);
+        a = p;
+        v = w;
+    }
+#ifdef CCL_STATS
+    atomicAdd(&g_stat_hops, hops);
+    atomicMax(&g_stat_maxhops, hops);
+    CCL_TASKSTAT(1, unsigned(hops));
+#endif
+    return v;
+}
+
+__device__ __forceinline__ void union_e(uint64_t* G, unsigned a, unsigned b) {
+    CCL_STAT(g_stat_unions);
+    CCL_LOOP_GUARD(ue);
+    while (true) {
+        CCL_LOOP_TICK(ue);
+        CCL_STAT(g_stat_steps);
+        CCL_TASKSTAT(0, 1u);
+        uint64_t va = find_e(G, a), vb = find_e(G, b);
+        if (va == vb) return;  // one root (distinct roots have distinct raster indices)
+        if (va < vb) { const uint64_t t = va; va = vb; vb = t; }
+        const uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(G + unsigned(va)),
+                                       static_cast<unsigned long long>(vb));
+        if (old == va) return;  // va's root was still a root: linked under vb's
+        CCL_TASKSTAT(2, 1u);
+        a = unsigned(old);  // it had been re-linked: union what the atomicMin displaced
+        b = unsigned(vb);
+    }
+}
+
+// Read-only find over edge slots after all unions (L2 loads).
+__device__ __forceinline__ uint64_t find_e_ro(const uint64_t* G, unsigned a) {
+    uint64_t v = __ldcg(reinterpret_cast<const unsigned long long*>(G) + a);
+    CCL_LOOP_GUARD(fer);
+    while (unsigned(v) != a) {
+        CCL_LOOP_TICK(fer);
+        a = unsigned(v);
+        v = __ldcg(reinterpret_cast<const unsigned long long*>(G) + a);
+    }
+    return v;
+}
+
 // Warp-cooperative union of a batch of root pairs: each lane holds at most one
 // pair (a, b) (a < 0: none).  Pairs already seen in this warp are dropped
 // (identical root pairs are common: two large components meet at many places
 // along a tile edge) so only one lane per distinct pair runs the union.
 template <bool NOUNION = false>
-__device__ __forceinline__ void warp_union_pairs(int32_t* G, int a, int b, unsigned long long& last) {
+__device__ __forceinline__ void warp_union_pairs(uint64_t* G, int a, int b, unsigned long long& last) {
     if (a > b) { int t = a; a = b; b = t; }
     const unsigned long long key =
         (a >= 0 && a != b) ? ((unsigned long long)(unsigned)a << 32) | (unsigned)b : ~0ull;
     const unsigned grp = __match_any_sync(kFull, key);
     const int lane = threadIdx.x & 31;
-    if (!NOUNION && key != ~0ull && key != last && (__ffs(grp) - 1) == lane) union_g(G, a, b);
+    if (!NOUNION && key != ~0ull && key != last && (__ffs(grp) - 1) == lane) union_e(G, unsigned(a), unsigned(b));
     if (key != ~0ull) last = key;
+}
+
+// edge slot of a K1 run record's root (boundary-row runs always carry a tag)
+__device__ __forceinline__ int rec_slot(uint32_t rec, unsigned ntiles, size_t t) {
+    CCL_ASSERT((rec >> 16) != 0);
+    return int(edge_slot(ntiles, int(rec >> 16) - 1, unsigned(t)));
 }
 
 // image-local raster index of a K1 run record's root (tile origin x0, y0)
@@ -1075,7 +1190,7 @@ constexpr int kPairsPerLane = CCL_PAIRS_PER_LANE;  // boundary pairs a lane cont
 
 template <int TY, int CONN, bool NOUNION = false>
 __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, const uint32_t* R,
-                                           const int32_t* E, int32_t* G, int b, int band, int tx,
+                                           const int32_t* E, uint64_t* G, int b, int band, int tx,
                                            Word (*s_w)[kWords], int2* pairs, int sub = 0, int sub_log2 = 0) {
     const int lane = threadIdx.x & 31;
     constexpr int RCAP = runs_per_tile_cap<TY>();
@@ -1083,21 +1198,34 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     const size_t t_lo = tile_index(g, b, band, tx);  // tile below the edge
     const size_t t_up = t_lo - g.tiles_x;             // tile above
     const uint32_t* bm = bits + size_t(b) * size_t(g.nwords);
-    int32_t* Gb = G + size_t(b) * size_t(g.npx);
     const uint32_t* Rlo = R + t_lo * RCAP;  // row 0 runs start at run id 0
-    const int up_base = __ldcg(E + t_up * kEdgeCap + 1);
-    CCL_ASSERT(up_base >= 0 && up_base < RCAP);
-    const uint32_t* Rup = R + t_up * RCAP + up_base;  // last row's runs
+    const int32_t* Elo = E + t_lo * kEdgeCap;
+    const int32_t* Eup = E + t_up * kEdgeCap;
+    const bool has_l = tx > 0, has_r = x0 + kTileW < g.W;
+    // ---- one round trip for the task's inputs: the two facing mask rows, the
+    // first 32 run records of each facing row (from the edge briefs), the
+    // corner words and column-root slots, the upper tile's last-row run base
+    // (only needed beyond 32 runs in a row)
+    const int up_base = __ldcg(Eup + 1);
     const int wg = tx * kWords + lane;
     const uint32_t* rowc = bm + size_t(y0) * g.WW;
     const uint32_t* rowu = rowc - g.WW;
     const uint32_t cur = wg < g.WW ? __ldcg(rowc + wg) : 0u;
     const uint32_t up = wg < g.WW ? __ldcg(rowu + wg) : 0u;
-    // the words diagonally across the tile corners, loaded with the rows (no
-    // second round trip): upper row, word left of the tile / right of it
+    const uint32_t r0 = uint32_t(__ldcg(Elo + kEdgeR0 + lane));  // records of the lower tile's top-row runs 0..31
+    const uint32_t rl = uint32_t(__ldcg(Eup + kEdgeRL + lane));  // ... of the upper tile's last-row runs 0..31
     uint32_t corner = 0;
-    if (CONN == 8 && lane == 0 && tx > 0) corner = __ldcg(rowu + wg - 1);
-    if (CONN == 8 && lane == 31 && x0 + kTileW < g.W) corner = __ldcg(rowu + wg + 1);
+    int ca = -1, cb = -1;  // tile-corner diagonal pair: slots straight from the column-root lists
+    if (CONN == 8 && lane == 0 && has_l) {
+        corner = __ldcg(rowu + wg - 1);
+        ca = __ldcg(Elo + kEdgeLC);
+        cb = __ldcg(Eup - kEdgeCap + kEdgeRC + TY - 1);
+    }
+    if (CONN == 8 && lane == 31 && has_r) {
+        corner = __ldcg(rowu + wg + 1);
+        ca = __ldcg(Elo + kEdgeRC);
+        cb = __ldcg(Eup + kEdgeCap + kEdgeLC + TY - 1);
+    }
     uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
     uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
     if (lane == 0) { curL = 0; upL = 0; }
@@ -1120,18 +1248,18 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     const uint32_t o = cur & up, oL = curL & upL;
     uint32_t ev = o & ~((o << 1) | (oL >> 31));
     uint32_t ne = 0, nw = 0;
-    bool cnw = false, cne = false;  // diagonal edges through the tile corners
+    bool corner_pair = false;
     if (CONN == 8) {
         const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
         const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
         ne = cur & ~cur_n & ~up & up_n;
         nw = cur & ~cur_p & ~up & up_p;
-        if (lane == 0 && tx > 0 && (cur & 1u)) cnw = corner >> 31;
-        if (lane == 31 && x0 + kTileW < g.W && (cur >> 31)) cne = corner & 1u;
+        if (lane == 0 && has_l && (cur & 1u)) corner_pair = (corner >> 31) != 0;   // (x0, y0) -- (x0-1, y0-1)
+        if (lane == 31 && has_r && (cur >> 31)) corner_pair = (corner & 1u) != 0;  // (x0+1023, y0) -- (x0+1024, y0-1)
     }
     if ((lane >> (5 - sub_log2)) != sub) {  // another warp's share of this boundary
         ev = ne = nw = 0;
-        cnw = cne = false;
+        corner_pair = false;
     }
     // run index (within its row) of the run containing foreground pixel x:
     // (number of run starts at positions <= x) - 1
@@ -1142,15 +1270,15 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         CCL_ASSERT(i >= 0 && i < kTileW / 2);
         return i;
     };
-    const int W = g.W;
     unsigned long long last = ~0ull;
-    // Rounds: every lane turns up to kPairsPerLane of its events into root
+    warp_union_pairs<NOUNION>(G, corner_pair ? ca : -1, cb, last);
+    // Rounds: every lane turns up to kPairsPerLane of its events into slot
     // pairs in the warp's shared list; the list is then unioned with the pairs
     // spread over all 32 lanes (a lane with many events no longer serialises
     // the warp's union latency).
-    while (__any_sync(kFull, ev | ne | nw | cnw | cne)) {
+    while (__any_sync(kFull, ev | ne | nw)) {
         if (lane == 0) CCL_TASKSTAT(3, 1u);
-        const int have = __popc(ev) + __popc(ne) + __popc(nw) + int(cnw) + int(cne);
+        const int have = __popc(ev) + __popc(ne) + __popc(nw);
         const int take = min(have, kPairsPerLane);
         int incl = take;
 #pragma unroll
@@ -1160,53 +1288,45 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         }
         const int total = __shfl_sync(kFull, incl, 31);
         const int pos = incl - take;
-        // all of this lane's record loads are issued before any is used (one
-        // round trip per round instead of one per event)
-        uint32_t va[kPairsPerLane], vc[kPairsPerLane];
-        unsigned raw = 0;  // bit e: the pair is two roots already (tile-corner diagonals)
+        int ia[kPairsPerLane], ib[kPairsPerLane];
 #pragma unroll
         for (int e = 0; e < kPairsPerLane; ++e) {
+            ia[e] = ib[e] = 0;
             if (e < take) {
-                if (ev | ne | nw) {
-                    int x, xu;
-                    if (ev) {
-                        x = (lane << 5) + __ffs(ev) - 1;
-                        ev &= ev - 1;
-                        xu = x;
-                    } else if (ne) {
-                        x = (lane << 5) + __ffs(ne) - 1;
-                        ne &= ne - 1;
-                        xu = x + 1;
-                    } else {
-                        x = (lane << 5) + __ffs(nw) - 1;
-                        nw &= nw - 1;
-                        xu = x - 1;
-                    }
-                    va[e] = __ldcg(Rlo + run_idx(0, x));
-                    vc[e] = __ldcg(Rup + run_idx(1, xu));
-                } else if (cnw) {  // (x0, y0) -- (x0-1, y0-1): right column of the upper-left tile
-                    cnw = false;
-                    va[e] = uint32_t(__ldcg(E + t_lo * kEdgeCap + kEdgeLC));
-                    vc[e] = uint32_t(__ldcg(E + (t_up - 1) * kEdgeCap + kEdgeRC + TY - 1));
-                    raw |= 1u << e;
-                } else {  // cne: (x0+1023, y0) -- (x0+1024, y0-1): left column of the upper-right tile
-                    cne = false;
-                    va[e] = uint32_t(__ldcg(E + t_lo * kEdgeCap + kEdgeRC));
-                    vc[e] = uint32_t(__ldcg(E + (t_up + 1) * kEdgeCap + kEdgeLC + TY - 1));
-                    raw |= 1u << e;
+                int x, xu;
+                if (ev) {
+                    x = (lane << 5) + __ffs(ev) - 1;
+                    ev &= ev - 1;
+                    xu = x;
+                } else if (ne) {
+                    x = (lane << 5) + __ffs(ne) - 1;
+                    ne &= ne - 1;
+                    xu = x + 1;
+                } else {
+                    x = (lane << 5) + __ffs(nw) - 1;
+                    nw &= nw - 1;
+                    xu = x - 1;
                 }
+                ia[e] = run_idx(0, x);
+                ib[e] = run_idx(1, xu);
             }
+        }
+        // records of runs 0..31 of either row from the briefs (shuffles);
+        // beyond that from the record lists (loads issued together)
+        uint32_t va[kPairsPerLane], vb[kPairsPerLane];
+#pragma unroll
+        for (int e = 0; e < kPairsPerLane; ++e) {
+            va[e] = __shfl_sync(kFull, r0, ia[e] & 31);
+            vb[e] = __shfl_sync(kFull, rl, ib[e] & 31);
         }
 #pragma unroll
         for (int e = 0; e < kPairsPerLane; ++e) {
-            if (e < take) {
-                const bool r = (raw >> e) & 1u;
-                const int a = r ? int(va[e]) : rec_root(va[e], W, x0, y0);
-                const int c = r ? int(vc[e]) : rec_root(vc[e], W, x0, y0 - TY);
-                CCL_ASSERT(a >= 0 && a < g.npx && c >= 0 && c < g.npx);
-                pairs[pos + e] = make_int2(a, c);
-            }
+            if (e < take && ia[e] >= kRL) va[e] = __ldcg(Rlo + ia[e]);
+            if (e < take && ib[e] >= kRL) vb[e] = __ldcg(R + t_up * RCAP + up_base + ib[e]);
         }
+#pragma unroll
+        for (int e = 0; e < kPairsPerLane; ++e)
+            if (e < take) pairs[pos + e] = make_int2(rec_slot(va[e], g.ntiles, t_lo), rec_slot(vb[e], g.ntiles, t_up));
         __syncwarp();
 #ifdef CCL_K2_PHASES
         if (g_k2_phase && lane == 0 && g_k2_phase[4 * size_t(ptask) + 1] == 0) g_k2_phase[4 * size_t(ptask) + 1] = gtimer();
@@ -1214,7 +1334,7 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
         for (int base = 0; base < total; base += 32) {
             const int i = base + lane;
             const int2 pr = i < total ? pairs[i] : make_int2(-1, -1);
-            warp_union_pairs<NOUNION>(Gb, pr.x, pr.y, last);
+            warp_union_pairs<NOUNION>(G, pr.x, pr.y, last);
 #ifdef CCL_K2_PHASES
             __syncwarp();
             if (g_k2_phase && lane == 0 && g_k2_phase[4 * size_t(ptask) + 2] == 0) g_k2_phase[4 * size_t(ptask) + 2] = gtimer();
@@ -1233,17 +1353,17 @@ template <int TY>
 __host__ __device__ constexpr int v_bands() { return 32 / TY; }
 
 template <int TY, int CONN>
-__device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, int32_t* G, int b, int band0,
+__device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, uint64_t* G, int b, int band0,
                                            int bx) {
     const int lane = threadIdx.x & 31;
     const int band = band0 + lane / TY, r = lane % TY;
-    int32_t* Gb = G + size_t(b) * size_t(g.npx);
+    uint64_t* Gb = G;  // edge slots are numbered over the whole batch
     int L = -1, Rr = -1;
     if (band < g.tiles_y && band * TY + r < g.H) {
         const int32_t* Er = E + tile_index(g, b, band, bx) * kEdgeCap;  // tile right of the edge
         const int32_t* El = Er - kEdgeCap;                               // tile left of the edge
-        L = __ldcg(El + kEdgeRC + r);   // root of (x0-1, y), or -1
-        Rr = __ldcg(Er + kEdgeLC + r);  // root of (x0, y), or -1
+        L = __ldcg(El + kEdgeRC + r);   // slot of the root of (x0-1, y), or -1
+        Rr = __ldcg(Er + kEdgeLC + r);  // slot of the root of (x0, y), or -1
     }
     unsigned long long last = ~0ull;
     warp_union_pairs(Gb, (L >= 0 && Rr >= 0) ? L : -1, Rr, last);        // W edge of (x0, y)
@@ -1261,7 +1381,7 @@ template <int TY, int CONN, int DBG = 0>
 __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
                                                   const uint32_t* __restrict__ R,
                                                   const int32_t* __restrict__ E,
-                                                  int32_t* __restrict__ G, long long n_h, long long n_v,
+                                                  uint64_t* __restrict__ G, long long n_h, long long n_v,
                                                   int sub_log2 = 0) {
     __shared__ Word s_w[8][2][kWords];
     __shared__ int2 s_pairs[8][32 * kPairsPerLane];
@@ -1308,7 +1428,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
-                                                             int32_t* __restrict__ G,
+                                                             uint64_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
                                                              int32_t* __restrict__ E,
                                                              void* __restrict__ k1x, unsigned ntiles) {
@@ -1343,32 +1463,33 @@ __global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const 
 // ~log d rounds instead of d dependent loads (the read-only walk left the
 // kernel waiting on a few 30+-hop chains).  Entries only ever move to
 // ancestors, so the forest stays valid for later readers.
+// Root entry (X << 32 | root) of edge slot s, with pointer jumping on s's own
+// entry (re-pointed at each grandparent read; only ancestors are ever stored).
+__device__ __forceinline__ uint64_t resolve_slot(uint64_t* G, unsigned s) {
+    uint64_t v = __ldcg(reinterpret_cast<const unsigned long long*>(G) + s);
+    if (unsigned(v) == s) return v;
+    CCL_LOOP_GUARD(pj);
+    while (true) {
+        CCL_LOOP_TICK(pj);
+        const uint64_t w = __ldcg(reinterpret_cast<const unsigned long long*>(G) + unsigned(v));
+        if (unsigned(w) == unsigned(v)) return w;  // v's parent is the root: w is the root's entry
+        CCL_ASSERT((w >> 32) < (v >> 32));
+        __stcg(reinterpret_cast<unsigned long long*>(G) + s, static_cast<unsigned long long>(w));
+        v = w;
+    }
+}
+
 template <int TY>
-__global__ void __launch_bounds__(256) k_resolve(Geom g, int32_t* __restrict__ G,
+__global__ void __launch_bounds__(256) k_resolve(Geom g, uint64_t* __restrict__ G,
                                                  const int32_t* __restrict__ E,
                                                  int32_t* __restrict__ F, unsigned ntiles) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
-    const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
     for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
-        const int32_t* Et = E + size_t(t) * kEdgeCap;
-        const int n = Et[0];
-        int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
+        const int n = E[size_t(t) * kEdgeCap];
         for (int i = lane; i < n; i += 32) {
-            const int x = Et[kEdgeList + i];
-            int p = __ldcg(Gb + x);
-            CCL_LOOP_GUARD(pj);
-            if (p != x) {
-                while (true) {
-                    CCL_LOOP_TICK(pj);
-                    const int gp = __ldcg(Gb + p);
-                    if (gp == p) break;
-                    CCL_ASSERT(gp < p);
-                    __stcg(Gb + x, gp);
-                    p = gp;
-                }
-            }
-            F[size_t(t) * kEdgeCap + i] = p + 1 + g.label_off;
+            const unsigned s = edge_slot(g.ntiles, i, t);
+            F[s] = int(resolve_slot(G, s) >> 32) + 1 + g.label_off;
         }
     }
 }
@@ -1408,7 +1529,7 @@ struct __align__(1024) LinkSmem {
     LWord wd[TY][kWords];
     int32_t lab[kLabCap];            // final label of tile run k (current row window)
     uint4 rc[kRunCache / 4];         // first run records of the tile (prefetched)
-    int32_t fl[2][kEdgeCap - kEdgeList];  // final labels of the edge roots of tiles j, j+1 (helper warp)
+    int32_t fl[2][edge_slots(TY)];   // final labels of the edge roots of tiles j, j+1 (helper warp)
     int32_t produced;                // tiles whose fl slot the helper warp has filled
     int32_t consumed;                // tiles whose fl slot the compute warps are done with
     int32_t rcnt[TY];
@@ -1625,8 +1746,6 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
     {
         const int total = __shfl_sync(kFull, v, TY - 1);
         for (int i = tid; i < (total + 31) / 32; i += kThreads) l2_discard(Rt + 32 * i);
-        if (tid == kThreads - 1 && total <= runs_per_tile_cap<TY>() - kRL)
-            l2_discard(Rt + runs_per_tile_cap<TY>() - kRL);  // the last-row copy (K2's fixed-offset slot)
         if ((W & 1023) == 0 && lane < TY / kWarps) {
             const int y = y0 + warp + lane * kWarps;
             if (y < g.H)
@@ -1650,31 +1769,14 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
 constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
 
 template <bool RES>
-__device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, int32_t* G,
+__device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, uint64_t* G,
                                                 const int32_t* F, unsigned t, int first, int stride) {
-    const int32_t* Et = E + size_t(t) * kEdgeCap;
-    const int n = __ldcg(Et);
+    const int n = __ldcg(E + size_t(t) * kEdgeCap);
     if (RES) {
-        const unsigned per_img = unsigned(g.tiles_x) * unsigned(g.tiles_y);
-        int32_t* Gb = G + size_t(t / per_img) * size_t(g.npx);
-        for (int i = first; i < n; i += stride) {
-            const int x = __ldcg(Et + kEdgeList + i);
-            int p = __ldcg(Gb + x);
-            CCL_LOOP_GUARD(pj);
-            if (p != x) {
-                while (true) {
-                    CCL_LOOP_TICK(pj);
-                    const int gp = __ldcg(Gb + p);
-                    if (gp == p) break;
-                    CCL_ASSERT(gp < p);
-                    __stcg(Gb + x, gp);
-                    p = gp;
-                }
-            }
-            slot[i] = p + 1 + g.label_off;
-        }
+        for (int i = first; i < n; i += stride)
+            slot[i] = int(resolve_slot(G, edge_slot(g.ntiles, i, t)) >> 32) + 1 + g.label_off;
     } else {
-        for (int i = first; i < n; i += stride) slot[i] = __ldcg(F + size_t(t) * kEdgeCap + i);
+        for (int i = first; i < n; i += stride) slot[i] = __ldcg(F + edge_slot(g.ntiles, i, t));
     }
 }
 
@@ -1685,7 +1787,7 @@ __device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, co
 // The helper warp's loop over the block's tiles j0, j0+1, ... (t = blockIdx.x
 // + j * gridDim.x).
 template <int TY, bool RES>
-__device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const int32_t* E, int32_t* G,
+__device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const int32_t* E, uint64_t* G,
                                           const int32_t* F, unsigned ntiles, int j0) {
     const int lane = threadIdx.x & 31;
     int j = j0;
@@ -1708,7 +1810,7 @@ template <int TY, int CONN, bool VEC, bool TMA = false, bool RES = true, int DBG
 __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* __restrict__ bits,
                                                         const uint32_t* __restrict__ R,
                                                         const int32_t* __restrict__ E,
-                                                        int32_t* __restrict__ G,
+                                                        uint64_t* __restrict__ G,
                                                         const int32_t* __restrict__ F,
                                                         int32_t* __restrict__ out, unsigned ntiles,
                                                         const __grid_constant__ CUtensorMap tmap) {

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) k_strip_mark(Geom g, const int32_t* __res
     const int lane = threadIdx.x & 31;
     for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
         const int n = E[size_t(t) * kEdgeCap];
-        for (int i = lane; i < n; i += 32) Gs[F[size_t(t) * kEdgeCap + i] - 1 - g.label_off] = -1;
+        for (int i = lane; i < n; i += 32) Gs[F[edge_slot(g.ntiles, i, t)] - 1 - g.label_off] = -1;
     }
 }
 
@@ -66,7 +66,6 @@ __global__ void __launch_bounds__(256) k_strip_edges(Geom g, const uint32_t* __r
     }
     const int pad = incl - __popc(s);
     const uint32_t* Rt = R + t * runs_per_tile_cap<TY>();
-    const int32_t* Ft = F + t * kEdgeCap;
     const int x0 = tx * kTileW;
     for (int bit = 0; bit < 32; ++bit) {
         const int x = x0 + (lane << 5) + bit;
@@ -76,7 +75,7 @@ __global__ void __launch_bounds__(256) k_strip_edges(Geom g, const uint32_t* __r
             const int idx = pad + __popc(s & (kFull >> (31 - bit))) - 1;
             const uint32_t rec = Rt[rbase + idx];
             const int e = int(rec >> 16), rr = int(rec & 0x7FFFu);
-            lab = e ? Ft[e - 1] : (band * TY + (rr >> 10)) * g.W + x0 + (rr & 1023) + 1 + g.label_off;
+            lab = e ? F[edge_slot(g.ntiles, e - 1, unsigned(t))] : (band * TY + (rr >> 10)) * g.W + x0 + (rr & 1023) + 1 + g.label_off;
             Gs[lab - 1 - g.label_off] = INT_MAX;
         }
         send[which * g.W + x] = lab;
@@ -149,7 +148,7 @@ __global__ void __launch_bounds__(256) k_strip_patch(Geom g, const int32_t* __re
     for (unsigned t = (blockIdx.x * 256u + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * 256u) >> 5) {
         const int n = E[size_t(t) * kEdgeCap];
         for (int i = lane; i < n; i += 32) {
-            int32_t* f = F + size_t(t) * kEdgeCap + i;
+            int32_t* f = F + edge_slot(g.ntiles, i, t);
             const int v = Gs[*f - 1 - g.label_off];
             if (v >= 0) *f = minlab[find_g_ro(P, slot0 + v)];
         }

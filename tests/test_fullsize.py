@@ -32,6 +32,15 @@ C5 = 32768
 
 
 @pytest.fixture(scope="module")
+def ccl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1708_08180_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
 def c5_image():
     return synth.upscaled_rows(C5, C5, 5001, 0, C5)
 

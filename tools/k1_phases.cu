@@ -41,7 +41,7 @@ __global__ void write_floor(int32_t* p, size_t n4) {
 // blocks, the edge roots' parent sectors) so they are L2-resident: isolates
 // how much of K2's time is DRAM latency on K1's outputs.
 __global__ void touch_k1_outputs(const uint32_t* bits, size_t nwords, const uint32_t* R, int rcap,
-                                 const int32_t* E, const int32_t* G, unsigned ntiles, unsigned* sink) {
+                                 const int32_t* E, const uint64_t* G, unsigned ntiles, unsigned* sink) {
     unsigned acc = 0;
     const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x, nt = size_t(gridDim.x) * blockDim.x;
     for (size_t i = tid; i < nwords; i += nt) acc ^= __ldcg(bits + i);
@@ -49,8 +49,8 @@ __global__ void touch_k1_outputs(const uint32_t* bits, size_t nwords, const uint
     for (size_t t = tid; t < ntiles; t += nt) {
         const int32_t* Et = E + t * ccl::kEdgeCap;
         const int n = __ldcg(Et);
-        for (int j = 0; j < ccl::kEdgeList + n && j < ccl::kEdgeCap; ++j) acc ^= __ldcg(Et + j);
-        for (int j = 0; j < n; ++j) acc ^= __ldcg(G + __ldcg(Et + ccl::kEdgeList + j));
+        for (int j = 0; j < ccl::kEdgeCap; ++j) acc ^= __ldcg(Et + j);
+        for (int j = 0; j < n; ++j) acc ^= unsigned(__ldcg(reinterpret_cast<const unsigned long long*>(G) + ccl::edge_slot(ntiles, j, unsigned(t))));
     }
     if (acc == 0x12345678u) sink[0] = acc;
 }
@@ -76,7 +76,7 @@ float timeit(F f, void* flush, size_t flush_bytes, int iters = 20) {
 }
 
 template <int TY, int CONN, int DBG>
-void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, int32_t* G, uint32_t* R,
+void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, uint64_t* G, uint32_t* R,
             int32_t* E, unsigned ntiles, int grid, void* flush, size_t fb) {
     auto k = ccl::k_local_merge<TY, CONN, true, DBG>;
     size_t smem = sizeof(ccl::K1Smem<TY>);
@@ -100,19 +100,20 @@ int main(int argc, char** argv) {
     }
     fclose(f);
     uint8_t* img;
-    int32_t *G, *out;
+    uint64_t* G;
+    int32_t* out;
     uint32_t* bits;
     uint32_t* R;
     int32_t *E, *F;
     void* flush;
     const size_t fb = size_t(512) << 20;
     CK(cudaMalloc(&img, n));
-    CK(cudaMalloc(&G, n * 4));
+    CK(cudaMalloc(&G, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 8));
     CK(cudaMalloc(&out, n * 4));
     CK(cudaMalloc(&bits, n / 8 + 4096));
     CK(cudaMalloc(&R, 2 * n + 65536));
     CK(cudaMalloc(&E, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
-    CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
+    CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 4));
     CK(cudaMalloc(&flush, fb));
     CK(cudaMalloc(&g_k1x, size_t(1024) * ccl::k1x_slot_bytes<32>()));
     unsigned* sink;
@@ -147,6 +148,7 @@ int main(int argc, char** argv) {
     g.div_vg = ccl::FastDiv((g.tiles_y + 32 / TY - 1) / (32 / TY));
     g.label_off = g.force_top = g.force_bottom = 0;
     g.k3_early = 1;
+    g.ntiles = ntiles;
     for (int per_sm : {4, 5}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
