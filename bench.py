@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the other C3 inputs / C2 d=0.5 reported beside the C3 headline")
     return ap.parse_args()
 
 
@@ -267,6 +269,47 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def variant_lines(args, ccl, dev, peak):
+    """The other C3 inputs (blobs, upscaled, i.i.d. noise d = 1/2, noise at
+    the percolation threshold) and C2 (2048^2 noise d = 1/2), each timed like
+    the headline (L2 flushed, CUDA events, mean of the steps), reported as
+    extra keys of the C3 line (the cost depends on the image)."""
+    import torch
+    import synth
+    conn = args.conn
+    cases = [("c3_blobs", lambda: synth.blobs(8192, 8192, seed=3002)),
+             ("c3_upscaled", lambda: synth.upscaled(8192, 8192, seed=3003)),
+             ("c3_noise", lambda: synth.noise(8192, 8192, 0.5, seed=3004)),
+             ("c3_perc", lambda: synth.noise(8192, 8192, synth.percolation_density(conn), seed=3005)),
+             ("c2_noise", lambda: synth.noise(2048, 2048, 0.5, seed=105))]
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    res = {}
+    for key, gen in cases:
+        img = torch.from_numpy(gen()).to(dev)
+        H, W = img.shape
+        out = torch.empty((H, W), dtype=torch.int32, device=dev)
+        ws = ccl.Workspace(1, H, W, conn, device=dev)
+        for _ in range(3):
+            flush.zero_()
+            ccl.label(img, conn, out=out, workspace=ws, tile_rows=args.tile_rows)
+        evs = []
+        for _ in range(10):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ccl.label(img, conn, out=out, workspace=ws, tile_rows=args.tile_rows)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        ms = statistics.mean(x.elapsed_time(y) for x, y in evs)
+        gbs = PATH_BYTES_PER_PX * H * W / (ms / 1e3) / 1e9
+        res[key] = {"H": H, "W": W, "ms_per_step": round(ms, 5), "value": round(H * W / (ms / 1e3) / 1e6, 2),
+                    "unit": UNIT, "path_roofline_frac": round(gbs / peak, 4)}
+        del img, out, ws
+    return res
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_1708_08180_b200 as ccl
@@ -383,6 +426,8 @@ def run_ours(args, rank, world, local):
             line["roofline"] = {"kernel": dom, "bound": "latency", "achieved": None, "peak": peak,
                                 "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src}
     line["clocks"] = clk.summary()
+    if args.config == "C3" and (args.kind or "texture") == "texture" and world == 1 and not args.no_variants:
+        line["variants"] = variant_lines(args, ccl, dev, peak)
 
     # end-to-end through the C ABI with host buffers (pinned), copies timed
     if not args.no_e2e:
@@ -499,9 +544,9 @@ def run_c5(args, rank, world, local):
         "wall_ms_per_step_incl_flush": round(1e3 * wall / K, 4),
         "step_ms": {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),
                     "max": round(max(step_ms), 5)},
-        "gpu_launches": 12 * K,
-        "gpu_launches_note": "per step: strip_local 7 (K1, K2 boundary, K2 resolve, mark, edges, min, rep) + "
-                             "strip_finalize 5 (slot init/union/minlab, patch, K3); + NCCL all-gather",
+        "gpu_launches": 6 * K,
+        "gpu_launches_note": "per step: strip_local 4 (K1, K2 boundary, strip edges, strip reps) + "
+                             "strip_finalize 2 (slot union, K3 with the strip-final resolve); + NCCL all-gather",
         "path_roofline": {"bytes_per_px": PATH_BYTES_PER_PX, "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                           "frac": round(gbs / peak, 4)},
         "roofline": {"kernel": "whole strip path (per rank)", "bound": "hbm", "achieved": round(gbs, 1),

@@ -65,12 +65,13 @@ const char* ccl_status_string(ccl_status_t status);
 int ccl_last_cuda_error(void);
 
 /* Device workspace (bytes) needed by the *_async entry points for B images of
- * H x W: the global union-find parent array of the boundary analysis (one int32
- * per pixel, only tile-edge entries are ever touched), the bit-packed
- * foreground mask (one bit per pixel, rows padded to 32 px), per-run records,
- * per-tile edge blocks and resolved labels, and the K1 scratch slots for
- * run-dense tiles.  Sized for every tile configuration.
- * Returns 0 for invalid arguments. */
+ * H x W (about 3.7 bytes per pixel): the bit-packed
+ * foreground mask (one bit per pixel, rows padded to 32 px), per-run records
+ * (sized for the worst case, alternating pixels), per-tile edge briefs, the
+ * boundary analysis' union-find over edge slots (8 bytes per slot, one slot
+ * per edge-touching local root, at most 1040-1088 per tile), the strip marks,
+ * and the K1 scratch slots for run-dense tiles.  Sized for every tile
+ * configuration.  Returns 0 for invalid arguments. */
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
 
 /* Label one H x W image (device pointers).  Allocates its workspace stream-
@@ -97,8 +98,8 @@ ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H
 
 /* As ccl_label_batched_async with an explicit tile height (rows per K1 thread
  * block: 8, 16 or 32; 0 = library default: 16, or 8 when 16-row tiles would
- * number fewer than 592 = 148 SMs x 4, i.e. small images; CCL_TILE_AUTO=0 in
- * the environment pins the default to 16).  The tile width is fixed at 1024
+ * number fewer than 4 per SM of the current device, i.e. small images;
+ * CCL_TILE_AUTO=0 in the environment pins the default to 16).  The tile width is fixed at 1024
  * pixels (32 lanes x 32 px).  Output is identical for every tile config
  * ("config independence"); unsupported values -> CCL_ERR_CONFIG. */
 ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
@@ -109,10 +110,11 @@ ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64
 /* The three stages individually (same arguments as ccl_label_batched_cfg_async),
  * for per-kernel timing and stage tests.  They must be enqueued in this order on
  * one stream with the same workspace:
- *   ccl_stage_local_merge  K1: reads images; writes the bit-packed mask and the
- *                          tile-edge entries of the parent array (workspace).
+ *   ccl_stage_local_merge  K1: reads images; writes the bit-packed mask, the
+ *                          per-run records, the edge briefs and the initial
+ *                          edge-slot entries (workspace).
  *   ccl_stage_boundary     K2: unions every foreground edge that crosses a tile
- *                          boundary into the parent array (workspace only).
+ *                          boundary into the edge-slot union-find (workspace only).
  *   ccl_stage_link         K3: resolves the tile-edge roots to their final
  *                          labels (the last step of the boundary analysis,
  *                          done by K3's helper warps) and writes labels_out
@@ -188,7 +190,8 @@ ccl_status_t ccl_label_3d_async(const uint8_t* volumes, int64_t B, int64_t D, in
  *   x_min, y_min, x_max, y_max   inclusive bounding box
  *   sum_x, sum_y   coordinate sums (centroid = sum / area)
  * labels: device int32 [B][H][W], canonical (as ccl_label writes them -- any
- * other content gives meaningless but memory-safe output).  stats: device,
+ * other content gives meaningless but memory-safe output); 16-byte aligned
+ * labels with H*W % 4 == 0 take 128-bit loads, other layouts scalar ones.  stats: device,
  * B * max_components records (image b at b * max_components).  counts:
  * device int32[B], K_b; when K_b > max_components only the first
  * max_components records are written.  Workspace >= ccl_stats_workspace_bytes.
@@ -212,13 +215,17 @@ ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t
 int64_t ccl_boundary_work_items(int64_t B, int64_t H, int64_t W, int tile_rows,
                                 int64_t* horizontal_segments, int64_t* vertical_pixels);
 
-/* End-to-end entry (host buffers): copies h_images (B*H*W bytes) to the device,
- * runs the three kernels and copies the labels back into h_labels (B*H*W int32),
- * all enqueued on `stream` in row-band chunks so copies overlap compute.
- * d_scratch is caller-owned device memory of >= ccl_host_scratch_bytes() bytes.
- * Returns after enqueueing; the caller synchronises `stream` before reading
- * h_labels.  h_images/h_labels should be page-locked (cudaHostAlloc /
- * cudaHostRegister) for asynchronous copies. */
+/* End-to-end entry (host buffers): enqueues on `stream`, in order, the copy of
+ * h_images (B*H*W bytes) to the device, the three kernels, and the copy of the
+ * labels back into h_labels (B*H*W int32).  Within one call the copies and the
+ * kernels are serialised on `stream` (the kernels need the whole image and
+ * the labels are final only after K3); callers overlap consecutive calls by
+ * alternating two streams and scratch buffers, so one call's label copy runs
+ * during the next call's image copy and kernels (paper_1708_08180_b200.
+ * HostPipeline, bench.py's e2e).  d_scratch is caller-owned device memory of
+ * >= ccl_host_scratch_bytes() bytes.  Returns after enqueueing; the caller
+ * synchronises `stream` before reading h_labels.  h_images/h_labels should be
+ * page-locked (cudaHostAlloc / cudaHostRegister) for asynchronous copies. */
 size_t ccl_host_scratch_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
 ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H, int64_t W,
                                   int connectivity, int32_t* h_labels,
@@ -235,14 +242,17 @@ ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H,
  *   ccl_strip_local    (rank r) K1 + K2 on the strip; writes the 4*W-int send
  *                      buffer: [0, W) labels of the strip's first row, [W, 2W)
  *                      of its last row (0 = background), [2W, 4W) for each of
- *                      those 2W slots the first slot with the same label.
- *                      labels_out (rows * W int32, this rank's output) is used
- *                      as scratch and must be passed unchanged to finalize.
+ *                      those 2W slots the first slot with the same label
+ *                      (-1: background).  The workspace carries state to
+ *                      finalize (pass the same buffer, unchanged).
  *   caller             all-gather of the k send buffers into gathered
  *                      (k * 4 * W int32, rank order) -- e.g. ncclAllGather.
- *   ccl_strip_finalize (rank r) min-union over the k*2W slots (same-label slots
- *                      of a strip; 4-/8-adjacent slots across every strip cut),
- *                      patch the strip's edge-component labels, K3: labels_out.
+ *   ccl_strip_finalize (rank r) min-label union over the k*2W slots (same-label
+ *                      slots of a strip; 4-/8-adjacent slots across every strip
+ *                      cut); K3 writes labels_out, taking for each component on
+ *                      a strip boundary the minimum label of its slot set.
+ * Six launches per step: local = K1, K2, strip edges, strip reps; finalize =
+ * slot union (a min-label union-find over the k*2W slots), K3.
  * Workspace: >= ccl_strip_workspace_bytes(rows, W, k, connectivity), the same
  * buffer for both calls.  Errors as above; CCL_ERR_DIMS also for rank/k/row0
  * out of range. */

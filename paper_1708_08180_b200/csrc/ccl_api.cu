@@ -20,10 +20,24 @@ namespace {
 thread_local int g_last_cuda_error = 0;
 
 constexpr int kDefaultTileRows = 16;
-constexpr int64_t kSmallTiles = 148 * 4;  // below this many 16-row tiles: 8-row tiles
+constexpr int64_t kSmallTilesPerSM = 4;  // below this many 16-row tiles per SM: 8-row tiles
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// SMs of the current device (launch sizing)
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 1;
+    }
+    return cached[dev];
+}
 
 struct Plan {
     ccl::Geom g;
@@ -44,7 +58,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     if (st != CCL_OK) return st;
     if (tile_rows == 0) {
         // Default tile height: 16 rows; 8 when 16-row tiles would not give
-        // the persistent K1 grid (148 SMs x 4-5 blocks) a tile per block --
+        // the persistent K1 grid (SMs x 4-5 blocks) a tile per block --
         // small images are latency-bound per tile (C1 512^2 noise 74 -> 56 us,
         // C2 2048^2 noise 130 -> 102 us).  CCL_TILE_AUTO=0 disables the rule.
         static const bool autoty = [] {
@@ -52,7 +66,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
             return !(v && v[0] == '0');
         }();
         const int64_t tiles16 = B * ((W + ccl::kTileW - 1) / ccl::kTileW) * ((H + 15) / 16);
-        tile_rows = (autoty && tiles16 < kSmallTiles) ? 8 : kDefaultTileRows;
+        tile_rows = (autoty && tiles16 < kSmallTilesPerSM * sm_count()) ? 8 : kDefaultTileRows;
     }
     if (tile_rows != 8 && tile_rows != 16 && tile_rows != 32) return CCL_ERR_CONFIG;
     if (B > INT32_MAX) return CCL_ERR_DIMS;
@@ -74,6 +88,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.force_top = 0;
     p.g.force_bottom = 0;
     p.g.k3_early = 1;
+    p.g.strip = 0;
     p.g.ntiles = unsigned(int64_t(B) * p.g.tiles_x * p.g.tiles_y);
     // edge slots (the boundary analysis' union-find nodes, 8 B each) and their
     // resolved labels in strip mode (4 B each): edge_slots(TY) per tile, sized
@@ -230,9 +245,9 @@ struct StripCtx {
     int32_t* send = nullptr;            // this rank's 4W send buffer
     const int32_t* gathered = nullptr;  // k * 4W, rank order
     int k = 1, rank = 0;
-    int32_t* P = nullptr;               // k * 2W slot parents
-    int32_t* minlab = nullptr;          // k * 2W
+    uint64_t* P = nullptr;              // k * 2W slot union-find entries (ccl_strip.cuh)
 };
+
 
 // Resident blocks per device for the persistent kernels K1 (which = 1) and
 // K3 (which = 3): SMs x blocks per SM at full occupancy, cached per
@@ -248,7 +263,7 @@ int persistent_blocks(int which) {
     int sms = 0, b = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (which == 1)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::kThreads1,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ccl::k_local_merge<TY, CONN, VEC>, ccl::k1_threads<TY>(),
                                                       smem_bytes_k1<TY>());
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_kernel<TY, CONN, VEC, true, true>(), ccl::kK3Threads,
@@ -277,8 +292,8 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     void* k1x = reinterpret_cast<char*>(F) + p.F_bytes;
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::kThreads1, smem_bytes_k1<TY>(), s>>>(
-            img, g, bits, G, runs, E, k1x, unsigned(ntiles));
+        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::k1_threads<TY>(), smem_bytes_k1<TY>(), s>>>(
+            img, g, bits, G, runs, E, F, k1x, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
@@ -292,7 +307,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
             // 2 or 4 warps so the launch still fills the GPU (one task per
             // warp, ~5900 warps resident in one wave)
             int sub_log2 = 0;
-            while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= 148LL * 40) ++sub_log2;
+            while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= (long long)sm_count() * 40) ++sub_log2;
 #ifndef CCL_K2_DBG
 #define CCL_K2_DBG 0  // timing experiments only (tools/build_variant.sh): 3 = skip K2, 4 = no unions
 #endif
@@ -301,33 +316,24 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
                            (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v, sub_log2);
             if (e != cudaSuccess) return e;
         }
-        // the resolve step (edge roots -> final labels) runs in K3's helper
-        // warps; the strip stages need the labels in F before K3, so there it
-        // is its own launch
-        if (stages & kStripEdges) {
-            const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-            e = launch_pdl(ccl::k_resolve<TY>, rblocks, 256, 0, s, g, G, (const int32_t*)E, F, unsigned(ntiles));
-            if (e != cudaSuccess) return e;
-        }
+        // the resolve step (edge roots -> final labels) runs in K3's helper warps
     }
     if (stages & kStripEdges) {
-        // edge-root marks (Gs = out as scratch), boundary-row labels, slot reps
-        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-        ccl::k_strip_mark<TY><<<rblocks, 256, 0, s>>>(g, E, F, out, unsigned(ntiles));
-        ccl::k_strip_edges<TY><<<unsigned((2 * g.tiles_x + 7) / 8), 256, 0, s>>>(g, bits, runs, E, F, sc->send, out);
-        const unsigned sb = unsigned(std::min(1184, (2 * g.W + 255) / 256));
-        ccl::k_strip_min<<<sb, 256, 0, s>>>(sc->send, out, g.W, g.label_off);
-        ccl::k_strip_rep<<<sb, 256, 0, s>>>(sc->send, out, g.W, g.label_off);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        // boundary-row labels + first slot per root (F), then the send
+        // buffer's reps and the slot union-find's initial roots
+        e = launch_pdl(ccl::k_strip_edges<TY>, unsigned((2 * g.tiles_x + 7) / 8), 256, 0, s, g,
+                       (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, F, sc->send);
+        if (e != cudaSuccess) return e;
+        const int n = sc->k * 2 * g.W;
+        const unsigned sb = unsigned(std::min(sm_count() * 8, (n + 255) / 256));
+        e = launch_pdl(ccl::k_strip_rep, sb, 256, 0, s, sc->send, (const int32_t*)F, sc->P, g.W, n);
+        if (e != cudaSuccess) return e;
     }
     if (stages & kStripFinalize) {
+        // after the caller's all-gather (a plain launch: it must not overlap it)
         const int n = sc->k * 2 * g.W;
-        const unsigned sb = unsigned(std::min(1184, (n + 255) / 256));
-        ccl::k_slots_init<<<sb, 256, 0, s>>>(sc->P, sc->minlab, n);
+        const unsigned sb = unsigned(std::min(sm_count() * 8, (n + 255) / 256));
         ccl::k_slots_union<CONN><<<sb, 256, 0, s>>>(sc->gathered, sc->P, sc->k, g.W);
-        ccl::k_slots_minlab<<<sb, 256, 0, s>>>(sc->gathered, sc->P, sc->minlab, sc->k, g.W);
-        const unsigned rblocks = unsigned(std::min<long long>((ntiles + 7) / 8, 148LL * 16));
-        ccl::k_strip_patch<TY><<<rblocks, 256, 0, s>>>(g, E, F, out, sc->P, sc->minlab, sc->rank, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK3) {
@@ -342,16 +348,18 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         }
         // labels leave through TMA bulk-tensor stores when rows are 32-px
         // multiples (all bench configs); else 128-bit st.global.cs.  The
-        // helper warp resolves the edge roots (RES), or in strip mode takes
-        // the patched labels from F.
+        // helper warp resolves the edge roots; in strip mode (!res) roots on
+        // a strip boundary take their slot set's minimum label.
         CUtensorMap map;
         std::memset(&map, 0, sizeof(map));
         const bool tma = VEC && g.W % 32 == 0 && encode_label_map(&map, out, g);
         const bool res = !(stages & kStripFinalize);
+        ccl::StripFinal sf{};
+        if (!res) sf = ccl::StripFinal{F, sc->P, sc->gathered, g.W, sc->rank * 2 * g.W};
         auto k3 = tma ? (res ? k3_kernel<TY, CONN, VEC, true, true>() : k3_kernel<TY, CONN, VEC, true, false>())
                       : (res ? k3_kernel<TY, CONN, VEC, false, true>() : k3_kernel<TY, CONN, VEC, false, false>());
         e = launch_pdl(k3, grid3, ccl::kK3Threads, smem, s, g3, (const uint32_t*)bits, (const uint32_t*)runs,
-                       (const int32_t*)E, G, (const int32_t*)F, out, unsigned(ntiles), map);
+                       (const int32_t*)E, G, sf, out, unsigned(ntiles), map);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -393,7 +401,7 @@ template <int CONN>
 cudaError_t run_method(int method, const uint8_t* img, int B, int H, int W, int32_t* out, void* ws, cudaStream_t s) {
     namespace cb = ccl::base;
     const long long npx = (long long)H * W, n = npx * B;
-    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, 148LL * 16));
+    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, (long long)sm_count() * 16));
     int32_t* G = static_cast<int32_t*>(ws);
     if (method == CCL_METHOD_UF) {
         const dim3 grid((W + cb::kBX - 1) / cb::kBX, (H + cb::kBY - 1) / cb::kBY, B);
@@ -555,7 +563,7 @@ ccl_status_t ccl_label_equal_async(const uint8_t* images, int64_t B, int64_t H, 
     const dim3 grid(unsigned((W + cb::kBX - 1) / cb::kBX), unsigned((H + cb::kBY - 1) / cb::kBY), unsigned(B));
     const int nrows = int((H - 1) / cb::kBY), ncols = int(2 * ((W + cb::kBX - 1) / cb::kBX));
     const long long per = (long long)nrows * W + (long long)ncols * H;
-    const unsigned flat_blocks = unsigned(std::min<long long>((nn + 255) / 256, 148LL * 16));
+    const unsigned flat_blocks = unsigned(std::min<long long>((nn + 255) / 256, (long long)sm_count() * 16));
     if (connectivity == 4) {
         cb::k_uf_local<4, true><<<grid, dim3(cb::kBX, cb::kBY), 0, s>>>(images, int(H), int(W), npx, G);
         if (per > 0)
@@ -606,7 +614,7 @@ ccl_status_t ccl_label_3d_async(const uint8_t* volumes, int64_t B, int64_t D, in
         cv::k_vol_local<26><<<grid, blk, 0, s>>>(volumes, int(D), int(H), int(W), nvox, int(bz), G);
         cv::k_vol_boundary<26><<<gb, 256, 0, s>>>(volumes, int(D), int(H), int(W), nvox, G);
     }
-    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, 148LL * 16));
+    const unsigned flat_blocks = unsigned(std::min<long long>((n + 255) / 256, (long long)sm_count() * 16));
     ccl::base::k_link_flat<<<flat_blocks, 256, 0, s>>>(G, labels_out, n, nvox, 1);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
@@ -667,7 +675,7 @@ ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t
     cs::k_stats_scan<<<unsigned(B), 1024, 0, s>>>(cnt, nchunks, counts);
     cs::k_stats_rank<<<gc, cs::kT, 0, s>>>(labels, npx, int(W), nchunks, cnt, M, stats, max_components);
     const unsigned ablocks = unsigned(std::max<long long>(1, std::min<long long>((npx + 16 * cs::kT - 1) / (16 * cs::kT),
-                                                                                   std::max<long long>(1, 148LL * 8 / B))));
+                                                                                   std::max<long long>(1, (long long)sm_count() * 8 / B))));
     cs::k_stats_accum<<<dim3(ablocks, unsigned(B)), cs::kT, 0, s>>>(labels, npx, int(W), M, stats, max_components);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
@@ -755,7 +763,7 @@ static size_t align_up_c(size_t v) { return (v + 255) / 256 * 256; }
 size_t ccl_strip_workspace_bytes(int64_t rows, int64_t W, int k, int connectivity) {
     Plan p;
     if (k < 1 || make_plan(1, rows, W, connectivity, 0, p) != CCL_OK) return 0;
-    return p.total() + 2 * align_up_c(size_t(k) * 2 * size_t(W) * sizeof(int32_t));
+    return p.total() + align_up_c(size_t(k) * 2 * size_t(W) * sizeof(uint64_t));
 }
 
 static ccl_status_t strip_plan(int64_t rows, int64_t W, int64_t row0, int64_t H_total, int conn, int k,
@@ -767,6 +775,7 @@ static ccl_status_t strip_plan(int64_t rows, int64_t W, int64_t row0, int64_t H_
     ccl_status_t st = make_plan(1, rows, W, conn, 0, p);
     if (st != CCL_OK) return st;
     p.g.label_off = int(row0 * W);
+    p.g.strip = 1;
     p.g.force_top = row0 > 0;
     p.g.force_bottom = row0 + rows < H_total;
     return CCL_OK;
@@ -785,6 +794,7 @@ ccl_status_t ccl_strip_local(const uint8_t* strip, int64_t rows, int64_t W, int6
     StripCtx sc;
     sc.send = send;
     sc.k = k;
+    sc.P = reinterpret_cast<uint64_t*>(static_cast<char*>(workspace) + p.total());
     return run(p, connectivity, kK1 | kK2 | kStripEdges, strip, labels_out, workspace,
                static_cast<cudaStream_t>(stream), &sc);
 }
@@ -803,9 +813,7 @@ ccl_status_t ccl_strip_finalize(const int32_t* gathered, int k, int rank, int64_
     sc.gathered = gathered;
     sc.k = k;
     sc.rank = rank;
-    char* slots = static_cast<char*>(workspace) + p.total();
-    sc.P = reinterpret_cast<int32_t*>(slots);
-    sc.minlab = reinterpret_cast<int32_t*>(slots + align_up_c(size_t(k) * 2 * size_t(W) * sizeof(int32_t)));
+    sc.P = reinterpret_cast<uint64_t*>(static_cast<char*>(workspace) + p.total());
     return run(p, connectivity, kStripFinalize | kK3, nullptr, labels_out, workspace,
                static_cast<cudaStream_t>(stream), &sc);
 }

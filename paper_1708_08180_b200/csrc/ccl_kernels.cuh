@@ -30,6 +30,7 @@
 //    ~ 1 B (image) + 4 B (labels) + 1/4 B (mask) + edge entries.
 #pragma once
 #include <cassert>
+#include <climits>
 #include <cstdint>
 #include <cuda.h>  // CUtensorMap (TMA descriptors; encoded on the host in ccl_api.cu)
 #include <cuda_runtime.h>
@@ -50,8 +51,18 @@ constexpr int kTileW = 1024;   // pixels per tile row
 constexpr int kWords = 32;     // 32-bit mask words per tile row
 constexpr int kThreads = 256;  // threads per K1/K3 block
 constexpr int kWarps = kThreads / 32;
-constexpr int kThreads1 = 256;  // threads per K1 block (512 measured slower on texture, faster on noise)
-constexpr int kWarps1 = kThreads1 / 32;
+// K1 block size: 256 threads for 8- and 16-row tiles (5 blocks per SM); for
+// 32-row tiles 512 threads (16 warps, two rows each: the same register
+// prefetch of the next tile as 16-row tiles) and 2 blocks per SM, whose
+// 110 KB of shared memory hold the run lists of an i.i.d.-noise tile
+// (~8192 runs) instead of sending it to the global scratch path.
+#ifndef CCL_K1_T32
+#define CCL_K1_T32 256  // 512 measured: texture K1 49.7 -> 53.9 us, noise 2.0 -> 0.8 ms (profiles/r02_ab_k1_ty32_256_vs_512.txt)
+#endif
+template <int TY>
+__host__ __device__ constexpr int k1_threads() { return TY > 16 ? CCL_K1_T32 : 256; }
+template <int TY>
+__host__ __device__ constexpr int k1_warps() { return k1_threads<TY>() / 32; }
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
 
@@ -83,6 +94,7 @@ struct Geom {
     int force_bottom;  // the image's last row borders another strip
     int k3_early;      // K3 may read K1's outputs before its PDL wait (K1 finished before K3's predecessor)
     unsigned ntiles;   // tiles of the whole batch: the stride of the edge-slot numbering
+    int strip;         // strip mode (row-strip sharding): K1 also clears the strip marks F of its edge slots
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -460,11 +472,16 @@ struct __align__(16) WordE {
 #ifndef CCL_K1_BLOCKS
 #define CCL_K1_BLOCKS 5
 #endif
+__host__ __device__ constexpr int k1_cap32() { return CCL_K1_T32 == 512 ? 11776 : 3456; }
 template <int TY>
 __host__ __device__ constexpr int k1_cap() {
-    // TY = 32: 16 KB of row words; 3456 runs keep the block at 44 KB (5 per SM)
-    return TY * kTileW / 2 < (TY > 16 ? 3456 : CCL_K1_CAP16) ? TY * kTileW / 2 : (TY > 16 ? 3456 : CCL_K1_CAP16);
+    // TY = 32: 16 KB of row words; 512 threads: 11776 runs (110 KB, 2 blocks
+    // per SM); 256 threads: 3456 runs keep the block at 44 KB (5 per SM)
+    return TY * kTileW / 2 < (TY > 16 ? k1_cap32() : CCL_K1_CAP16) ? TY * kTileW / 2
+                                                                   : (TY > 16 ? k1_cap32() : CCL_K1_CAP16);
 }
+template <int TY>
+__host__ __device__ constexpr int k1_min_blocks() { return (TY > 16 && CCL_K1_T32 == 512) ? 2 : CCL_K1_BLOCKS; }
 template <int TY>
 __host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
 template <int TY>
@@ -592,11 +609,11 @@ __device__ __forceinline__ void k3_stamp(unsigned t, int k) {
 
 template <int TY>
 struct ImgRegs {
-    uint4 v[(TY + kWarps1 - 1) / kWarps1][2];  // row i of the warp: bytes 32*lane .. 32*lane + 31
+    uint4 v[(TY + k1_warps<TY>() - 1) / k1_warps<TY>()][2];  // row i of the warp: bytes 32*lane .. 32*lane + 31
 };
 
 template <int TY>
-__host__ __device__ constexpr bool k1_prefetches() { return TY <= 16; }
+__host__ __device__ constexpr bool k1_prefetches() { return (TY + k1_warps<TY>() - 1) / k1_warps<TY>() <= 2; }
 
 // One lane's 32 contiguous pixels of a tile row: one 256-bit load when the
 // row is 32-byte aligned (W % 32 == 0 and an aligned image), else two 128-bit
@@ -620,8 +637,8 @@ __device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, u
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
 #pragma unroll
-    for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
-        const int y = (warp + i * kWarps1 < TY) ? id.y0 + warp + i * kWarps1 : g.H;
+    for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
+        const int y = (warp + i * k1_warps<TY>() < TY) ? id.y0 + warp + i * k1_warps<TY>() : g.H;
         pf.v[i][0] = pf.v[i][1] = make_uint4(0, 0, 0, 0);
 #if CCL_K1_V8
         const int x = id.x0 + 32 * lane;
@@ -660,14 +677,15 @@ __device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uin
 template <int TY, int CONN, int DBG>
 __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ rs, uint16_t* __restrict__ re,
                                         int32_t* P, const Geom& g, unsigned t, const TileId& id, int v,
-                                        int total, uint64_t* G, uint32_t* R, int32_t* E, int warp, int lane) {
+                                        int total, uint64_t* G, uint32_t* R, int32_t* E, int32_t* F, int warp,
+                                        int lane) {
     const int tid = threadIdx.x;
     // run lists: rs / re in raster order of the starts (one loop over the
     // word's starts and ends together: starts and ends alternate, so a word
     // holds at most one more of either)
     {
-        for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
-            const int r = warp + i * kWarps1;
+        for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
+            const int r = warp + i * k1_warps<TY>();
             if (r >= TY) break;  // warp-uniform
             const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
             const WordE w = sm.wd[r][lane];
@@ -739,7 +757,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
 #if CCL_K1_RUNLOOP == 2 && !CCL_K1_UF2
         // P[k] = k for every run, four entries per 128-bit store
-        for (int k = 4 * tid; k < total; k += 4 * kThreads1)
+        for (int k = 4 * tid; k < total; k += 4 * k1_threads<TY>())
             *reinterpret_cast<int4*>(P + k) = make_int4(k, k + 1, k + 2, k + 3);
 #endif
     }
@@ -769,7 +787,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     // row and retried under contention: K1's union phase was 34 % of a
     // texture tile and 78 % of a noise tile.)
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
+    for (int k = tid; k < total; k += k1_threads<TY>()) {
         const int rsk = rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
         const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
@@ -786,7 +804,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     }
     __syncthreads();
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
+    for (int k = tid; k < total; k += k1_threads<TY>()) {
         const int rsk = rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
         if (r + 1 >= TY || k == 0) continue;
@@ -802,7 +820,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
 #else
     if (total > CCL_K1_DENSE) {
 #pragma unroll 1
-        for (int k = tid; k < total; k += kThreads1) {
+        for (int k = tid; k < total; k += k1_threads<TY>()) {
             const int rsk = rs[k];
             const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
             const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
@@ -820,7 +838,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         // (unsigned atomicMax; the low 16 bits of a root entry stay its id);
         // every other run is pointed straight at its root
 #pragma unroll 1
-        for (int k = tid; k < total; k += kThreads1) {
+        for (int k = tid; k < total; k += k1_threads<TY>()) {
             const int r = find_r_ro(P, k);
             if (r != k) P[k] = r;
             atomicMax(reinterpret_cast<unsigned*>(P + r), ((0xFFFFu - uint32_t(k)) << 16) | uint32_t(r));
@@ -828,7 +846,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         __syncthreads();
         // each root r hands its component to the minimum m: P[r] = m, P[m] = m
 #pragma unroll 1
-        for (int k = tid; k < total; k += kThreads1) {
+        for (int k = tid; k < total; k += k1_threads<TY>()) {
             const uint32_t v = uint32_t(P[k]);
             if (v >> 16) {  // a root (only roots carry the packed minimum; P[m] = m below clears it)
                 const int m = int(0xFFFFu - (v >> 16));
@@ -839,13 +857,13 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
         __syncthreads();
         // every run one hop further: its root's entry now names the minimum
 #pragma unroll 1
-        for (int k = tid; k < total; k += kThreads1) {
+        for (int k = tid; k < total; k += k1_threads<TY>()) {
             const int pk = P[k];
             if (pk != k) P[k] = P[pk];
         }
     } else {
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
+    for (int k = tid; k < total; k += k1_threads<TY>()) {
         const int rsk = rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
         const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
@@ -890,7 +908,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     const bool left = x0 > 0, right = x0 + kTileW < W;
     int32_t* Eh = E + size_t(t) * kEdgeCap;
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
+    for (int k = tid; k < total; k += k1_threads<TY>()) {
         const int root = find_r_ro(P, k);
         if (root != k) P[k] = root;  // an ancestor: concurrent finds stay valid
         const int rsk = rs[k];
@@ -928,7 +946,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     const int rb_last = sm.rbase[last_row];
     const int ne = sm.ecount;  // (read before the last barrier: the next tile resets it)
 #pragma unroll 1
-    for (int k = tid; k < total; k += kThreads1) {
+    for (int k = tid; k < total; k += k1_threads<TY>()) {
         const int root = P[k] & 0xFFFF;
         const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge index, or 0
         const uint32_t rec = uint32_t(rs[root]) | (uint32_t(tag) << 16);
@@ -948,7 +966,7 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
     // boundary analysis' loads and atomics hit fully valid L2 sectors
     {
 #pragma unroll 1
-        for (int j = tid; 4 * j < ne; j += kThreads1) {
+        for (int j = tid; 4 * j < ne; j += k1_threads<TY>()) {
             uint32_t v[8];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -965,6 +983,11 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             int4* sec = reinterpret_cast<int4*>(G + edge_slot(g.ntiles, 4 * j, t));
             st_keep_v4(sec, make_int4(int(v[0]), int(v[1]), int(v[2]), int(v[3])));
             st_keep_v4(sec + 1, make_int4(int(v[4]), int(v[5]), int(v[6]), int(v[7])));
+            if (g.strip) {  // strip marks: "no strip-boundary pixel seen yet" (ccl_strip.cuh)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (4 * j + q < ne) F[edge_slot(g.ntiles, 4 * j + q, t)] = -1;
+            }
         }
     }
 }
@@ -973,30 +996,32 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
 template <int TY, int CONN, bool VEC, int DBG = 0>
 __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
                                         ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
-                                        uint64_t* G, uint32_t* R, int32_t* E, void* k1x, int warp, int lane,
-                                        bool v8) {
+                                        uint64_t* G, uint32_t* R, int32_t* E, int32_t* F, void* k1x, int warp,
+                                        int lane, bool v8) {
     const TileId id = decode_tile<TY>(g, t);
     const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
     uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
     const int tid = threadIdx.x;
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 0);
 
+#if CCL_K1_V8
+    // tall tiles (no room to hold the next tile in registers across the whole
+    // tile): this warp's rows are loaded here, all before any is converted
+    // (their L2 round trips overlap; the next tile was pulled into L2 by the
+    // bulk prefetch below while this one was processed)
+    if (VEC && !k1_prefetches<TY>()) k1_prefetch<TY>(img, g, t, warp, lane, v8, cur);
+#endif
     // Alg. 1 l.3-8: the tile's pixels -> foreground masks (out-of-image pixels
     // read as background, R5)
 #pragma unroll
-    for (int i = 0; i < (TY + kWarps1 - 1) / kWarps1; ++i) {
-        const int r = warp + i * kWarps1;
+    for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
+        const int r = warp + i * k1_warps<TY>();
         if (r >= TY) break;  // warp-uniform
         const int y = id.y0 + r;
         uint32_t m = 0;
         if (VEC) {
             uint4 v0 = cur.v[i][0], v1 = cur.v[i][1];
 #if CCL_K1_V8
-            if (!k1_prefetches<TY>()) {  // tall tiles: load in place (register budget)
-                v0 = v1 = make_uint4(0, 0, 0, 0);
-                const int x = id.x0 + 32 * lane;
-                if (y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, v0, v1);
-            }
             // the lane's own 32 contiguous pixels: no cross-lane assembly
             m = nz16(v0) | (nz16(v1) << 16);
 #else
@@ -1034,7 +1059,7 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, v8, cur);
     // tall tiles (no register room for a second tile): the next tile's rows
     // are pulled into L2 with bulk prefetches instead, one per row
-    if (VEC && !k1_prefetches<TY>() && tnext < ntiles && warp == kWarps1 - 1 && lane < TY) {
+    if (VEC && !k1_prefetches<TY>() && tnext < ntiles && warp == k1_warps<TY>() - 1 && lane < TY) {
         const TileId nx = decode_tile<TY>(g, tnext);
         const int y = nx.y0 + lane;
         if (y < g.H) {
@@ -1060,12 +1085,12 @@ __device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, cons
     if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
     if (warp == 0 && lane == 0) sm.rbase[0] = 0;
     if (total <= k1_cap<TY>()) {
-        k1_runs<TY, CONN, DBG>(sm, sm.rs, sm.re, sm.P, g, t, id, v, total, G, R, E, warp, lane);
+        k1_runs<TY, CONN, DBG>(sm, sm.rs, sm.re, sm.P, g, t, id, v, total, G, R, E, F, warp, lane);
     } else {
         char* slot = static_cast<char*>(k1x) + size_t(blockIdx.x) * k1x_slot_bytes<TY>();
         constexpr int N = TY * kTileW / 2 + 8;
         k1_runs<TY, CONN, DBG>(sm, reinterpret_cast<uint16_t*>(slot), reinterpret_cast<uint16_t*>(slot) + N,
-                               reinterpret_cast<int32_t*>(slot + 4 * N), g, t, id, v, total, G, R, E, warp, lane);
+                               reinterpret_cast<int32_t*>(slot + 4 * N), g, t, id, v, total, G, R, E, F, warp, lane);
     }
 }
 
@@ -1426,11 +1451,12 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
 template <int TY, int CONN, bool VEC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const uint8_t* __restrict__ img, Geom g,
+__global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              uint64_t* __restrict__ G,
                                                              uint32_t* __restrict__ R,
                                                              int32_t* __restrict__ E,
+                                                             int32_t* __restrict__ F,
                                                              void* __restrict__ k1x, unsigned ntiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem<TY>& sm = *reinterpret_cast<K1Smem<TY>*>(smem_raw);
@@ -1445,7 +1471,7 @@ __global__ void __launch_bounds__(kThreads1, CCL_K1_BLOCKS) k_local_merge(const 
     ImgRegs<TY> a;
     if (PF) k1_prefetch<TY>(img, g, t, warp, lane, v8, a);
     while (t < ntiles) {
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, k1x, warp, lane, v8);
+        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, F, k1x, warp, lane, v8);
         t += gridDim.x;
     }
 }
@@ -1768,15 +1794,28 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
 // in F.  k3_resolve_tile does one tile's roots i = first, first + stride, ...
 constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
 
+// Strip mode (ccl_strip.cuh): the final label of an edge root on a strip
+// boundary row is the minimum label of its slot set in the slot union-find.
+struct StripFinal {
+    const int32_t* F;         // F[root slot] = INT_MAX - its first boundary slot, or -1
+    uint64_t* P;              // slot union-find over the k * 2W boundary slots
+    const int32_t* gathered;  // all ranks' send buffers (labels, reps)
+    int W, slot0;             // slot0 = this rank's first slot (rank * 2W)
+};
+__device__ __forceinline__ uint64_t slot_find(uint64_t* P, const int32_t* gathered, int W, unsigned s);
+
 template <bool RES>
 __device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, uint64_t* G,
-                                                const int32_t* F, unsigned t, int first, int stride) {
+                                                const StripFinal& sf, unsigned t, int first, int stride) {
     const int n = __ldcg(E + size_t(t) * kEdgeCap);
-    if (RES) {
-        for (int i = first; i < n; i += stride)
-            slot[i] = int(resolve_slot(G, edge_slot(g.ntiles, i, t)) >> 32) + 1 + g.label_off;
-    } else {
-        for (int i = first; i < n; i += stride) slot[i] = __ldcg(F + edge_slot(g.ntiles, i, t));
+    for (int i = first; i < n; i += stride) {
+        const uint64_t w = resolve_slot(G, edge_slot(g.ntiles, i, t));
+        int lab = int(w >> 32) + 1 + g.label_off;
+        if (!RES) {  // strip mode
+            const int v = __ldcg(sf.F + unsigned(w));
+            if (v >= 0) lab = int(slot_find(sf.P, sf.gathered, sf.W, unsigned(sf.slot0 + (INT_MAX - v))) >> 32);
+        }
+        slot[i] = lab;
     }
 }
 
@@ -1788,7 +1827,7 @@ __device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, co
 // + j * gridDim.x).
 template <int TY, bool RES>
 __device__ __forceinline__ void k3_helper(LinkSmem<TY>& sm, const Geom& g, const int32_t* E, uint64_t* G,
-                                          const int32_t* F, unsigned ntiles, int j0) {
+                                          const StripFinal& F, unsigned ntiles, int j0) {
     const int lane = threadIdx.x & 31;
     int j = j0;
     for (unsigned t = blockIdx.x + unsigned(j0) * gridDim.x; t < ntiles; t += gridDim.x, ++j) {
@@ -1811,7 +1850,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
                                                         const uint32_t* __restrict__ R,
                                                         const int32_t* __restrict__ E,
                                                         uint64_t* __restrict__ G,
-                                                        const int32_t* __restrict__ F,
+                                                        const StripFinal F,
                                                         int32_t* __restrict__ out, unsigned ntiles,
                                                         const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];

@@ -75,13 +75,14 @@ float timeit(F f, void* flush, size_t flush_bytes, int iters = 20) {
     return 1000.f * tot / iters;
 }
 
+static int32_t* g_F = nullptr;
 template <int TY, int CONN, int DBG>
 void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, uint64_t* G, uint32_t* R,
             int32_t* E, unsigned ntiles, int grid, void* flush, size_t fb) {
     auto k = ccl::k_local_merge<TY, CONN, true, DBG>;
     size_t smem = sizeof(ccl::K1Smem<TY>);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    float us = timeit([&] { k<<<grid, ccl::kThreads1, smem>>>(img, g, bits, G, R, E, g_k1x, ntiles); }, flush, fb);
+    float us = timeit([&] { k<<<grid, ccl::k1_threads<TY>(), smem>>>(img, g, bits, G, R, E, g_F, g_k1x, ntiles); }, flush, fb);
     printf("%-34s grid %6d  %8.1f us\n", name, grid, us);
 }
 
@@ -114,6 +115,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&R, 2 * n + 65536));
     CK(cudaMalloc(&E, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
     CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 4));
+    g_F = F;
     CK(cudaMalloc(&flush, fb));
     CK(cudaMalloc(&g_k1x, size_t(1024) * ccl::k1x_slot_bytes<32>()));
     unsigned* sink;
@@ -196,7 +198,7 @@ int main(int argc, char** argv) {
         float tot2 = 0;
         for (int i = 0; i < 23; ++i) {
             CK(cudaMemsetAsync(flush, i, fb));
-            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
             CK(cudaEventRecord(a));
             k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
             CK(cudaEventRecord(b));
@@ -223,7 +225,7 @@ int main(int argc, char** argv) {
         float tot2 = 0;
         for (int i = 0; i < 23; ++i) {
             CK(cudaMemsetAsync(flush, i, fb));
-            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
             touch_k1_outputs<<<sms * 4, 256>>>(bits, g.nwords, R, ccl::runs_per_tile_cap<TY>(), E, G, ntiles, sink);
             CK(cudaEventRecord(a));
             ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
@@ -247,7 +249,7 @@ int main(int argc, char** argv) {
         for (int ver = 0; ver < 1; ++ver) {
         CK(cudaMemset(ph, 0, size_t(nt) * 32));
         if (ver == 0) CK(cudaMemcpyToSymbol(ccl::g_k2_phase, &ph, sizeof(ph)));
-        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
         auto kt = ccl::k_boundary<TY, 8, 8>;
         kt<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
         CK(cudaDeviceSynchronize());
@@ -296,7 +298,7 @@ int main(int argc, char** argv) {
             CK(cudaMalloc(&ts, size_t(nt) * 16));
             CK(cudaMemset(ts, 0, size_t(nt) * 16));
             CK(cudaMemcpyToSymbol(ccl::g_k2_taskstat, &ts, sizeof(ts)));
-            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
             ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
             CK(cudaDeviceSynchronize());
             std::vector<unsigned> hts(size_t(nt) * 4);
@@ -322,7 +324,7 @@ int main(int argc, char** argv) {
         CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &np, sizeof(np)));
     }
     {
-        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         float us = timeit([&] { ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles); }, flush, fb);
         printf("%-34s %8.1f us\n", "K2b resolve", us);
@@ -333,7 +335,7 @@ int main(int argc, char** argv) {
         unsigned long long z = 0, u, st, nf, nh, mh;
         CK(cudaMemcpyToSymbol(ccl::g_stat_unions, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_steps, &z, 8));
-        k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpyToSymbol(ccl::g_stat_finds, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_hops, &z, 8));
@@ -351,7 +353,7 @@ int main(int argc, char** argv) {
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_unions, &z, 8));
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_steps, &z, 8));
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_hops, &z, 8));
-            k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
             CK(cudaDeviceSynchronize());
             CK(cudaMemcpyFromSymbol(&ku, ccl::g_stat_k1_unions, 8));
             CK(cudaMemcpyFromSymbol(&ks, ccl::g_stat_k1_steps, 8));
@@ -363,11 +365,11 @@ int main(int argc, char** argv) {
     }
 #endif
     // K3 (after K1 + K2), with stamps
-    k1<<<grid1, ccl::kThreads1, sm1>>>(img, g, bits, G, R, E, g_k1x, ntiles);
+    k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
     ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
-    auto k3 = ccl::k_link<TY, 8, true, true, false, 0>;
-    auto k3s = ccl::k_link<TY, 8, true, true, false, 4>;
+    auto k3 = ccl::k_link<TY, 8, true, true, true, 0>;
+    auto k3s = ccl::k_link<TY, 8, true, true, true, 4>;
     const size_t sm3 = sizeof(ccl::LinkSmem<TY>);
     CUtensorMap tmap;
     {
@@ -385,24 +387,24 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     CK(cudaFuncSetAttribute(k3s, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
     for (int grid3 : {370, 390, 410, 428, 444}) {
-        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
+        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, ccl::StripFinal{}, out, ntiles, tmap); }, flush, fb);
         printf("K3 grid %4d (%.2f tiles/block)     %8.1f us\n", grid3, double(ntiles) / grid3, us);
     }
     for (int per_sm : {3, 4, 5}) {
         const int grid3 = std::min<int>(ntiles, sms * per_sm);
-        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
+        float us = timeit([&] { k3<<<grid3, ccl::kK3Threads, sm3>>>(g, bits, R, E, G, ccl::StripFinal{}, out, ntiles, tmap); }, flush, fb);
         printf("K3 x%d                              %8.1f us\n", per_sm, us);
     }
     {
-        auto k3z = ccl::k_link<TY, 8, true, true, false, 1>;
+        auto k3z = ccl::k_link<TY, 8, true, true, true, 1>;
         CK(cudaFuncSetAttribute(k3z, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
-        float us = timeit([&] { k3z<<<std::min<int>(ntiles, sms * 3), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
+        float us = timeit([&] { k3z<<<std::min<int>(ntiles, sms * 3), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, ccl::StripFinal{}, out, ntiles, tmap); }, flush, fb);
         printf("K3 x3, no expansion (stale rowbuf)  %8.1f us\n", us);
     }
     unsigned long long* st3;
     CK(cudaMalloc(&st3, size_t(ntiles) * 8 * 8));
     CK(cudaMemcpyToSymbol(ccl::g_k3_stamps, &st3, sizeof(st3)));
-    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, F, out, ntiles, tmap); }, flush, fb);
+    float us3 = timeit([&] { k3s<<<std::min<int>(ntiles, sms * 4), ccl::kK3Threads, sm3>>>(g, bits, R, E, G, ccl::StripFinal{}, out, ntiles, tmap); }, flush, fb);
     printf("K3 + stamps x4                     %8.1f us\n", us3);
     CK(cudaMemcpy(hs.data(), st3, hs.size() * 8, cudaMemcpyDeviceToHost));
     const char* n3[3] = {"row runs", "label table", "expand+write"};
