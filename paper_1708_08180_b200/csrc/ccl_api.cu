@@ -14,6 +14,9 @@
 #include <cstring>
 #include <utility>
 #include <mutex>
+#include <atomic>
+#include <chrono>
+#include <random>
 
 namespace {
 
@@ -24,6 +27,17 @@ constexpr int64_t kSmallTilesPerSM = 4;  // below this many 16-row tiles per SM:
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// A value unique to this call (per process; 64-bit, randomly seeded): the
+// K1 -> K2 ready flags carry it, so flags left in a reused workspace by an
+// earlier call never read as ready.
+unsigned long long next_epoch() {
+    static std::atomic<unsigned long long> counter{
+        (std::random_device{}() * 0x9E3779B97F4A7C15ull) ^ (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count()};
+    unsigned long long e;
+    do { e = counter.fetch_add(0x9E3779B97F4A7C15ull) + 0x9E3779B97F4A7C15ull; } while (e == 0);
+    return e;
+}
 
 // SMs of the current device (launch sizing)
 int sm_count() {
@@ -42,8 +56,8 @@ int sm_count() {
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, k1x_bytes;
-    size_t total() const { return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + k1x_bytes; }
+    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, k1x_bytes, ready_bytes;
+    size_t total() const { return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + k1x_bytes + ready_bytes; }
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -89,6 +103,8 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.force_bottom = 0;
     p.g.k3_early = 1;
     p.g.strip = 0;
+    p.g.epoch = 0;
+    p.g.ready = nullptr;
     p.g.ntiles = unsigned(int64_t(B) * p.g.tiles_x * p.g.tiles_y);
     // edge slots (the boundary analysis' union-find nodes, 8 B each) and their
     // resolved labels in strip mode (4 B each): edge_slots(TY) per tile, sized
@@ -109,6 +125,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     // edge briefs E: kEdgeCap ints per tile, for the most tiles any config
     // makes (tile_rows = 8)
     p.edge_bytes = align_up(tiles8 * ccl::kEdgeCap * sizeof(int32_t));
+    p.ready_bytes = align_up(tiles8 * sizeof(uint64_t));  // per-tile ready flags (K1 -> K2 overlap)
     // K1 scratch slots for tiles over the shared-memory run capacity (one per
     // K1 block; tile_rows = 8 never overflows), sized for the larger need
     p.k1x_bytes = align_up(std::max(std::min(tiles16, size_t(ccl::k1x_slots<16>())) * ccl::k1x_slot_bytes<16>(),
@@ -277,7 +294,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
                        cudaStream_t s, const StripCtx* sc) {
     cudaError_t e = setup_attrs<TY, CONN, VEC>();
     if (e != cudaSuccess) return e;
-    const ccl::Geom& g = p.g;
+    ccl::Geom g = p.g;  // (per call: the K1 -> K2 overlap epoch below)
     uint64_t* G = static_cast<uint64_t*>(ws);
     uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes);
     uint32_t* runs = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p.G_bytes + p.bits_bytes);
@@ -291,6 +308,19 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)), ccl::k1x_slots<TY>()));
     void* k1x = reinterpret_cast<char*>(F) + p.F_bytes;
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
+    const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
+    const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
+                          (g.tiles_x - 1);
+    g.epoch = 0;
+    g.ready = nullptr;
+    static const bool overlap = [] {
+        const char* v = std::getenv("CCL_K1K2_OVERLAP");
+        return !(v && v[0] == '0');
+    }();
+    if (overlap && (stages & kK1) && (stages & kK2) && n_h + n_v > 0) {
+        g.epoch = next_epoch();
+        g.ready = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + p.total() - p.ready_bytes);
+    }
     if (stages & kK1) {
         ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::k1_threads<TY>(), smem_bytes_k1<TY>(), s>>>(
             img, g, bits, G, runs, E, F, k1x, unsigned(ntiles));
@@ -299,9 +329,6 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     if (stages & kK2) {
         // K2: boundary unions (one warp per tile boundary), then resolve every
         // tile's edge-touching roots (one warp per tile)
-        const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
-        const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
-                              (g.tiles_x - 1);
         if (n_h + n_v > 0) {
             // few boundaries (small images): split each horizontal one over
             // 2 or 4 warps so the launch still fills the GPU (one task per

@@ -95,6 +95,11 @@ struct Geom {
     int k3_early;      // K3 may read K1's outputs before its PDL wait (K1 finished before K3's predecessor)
     unsigned ntiles;   // tiles of the whole batch: the stride of the edge-slot numbering
     int strip;         // strip mode (row-strip sharding): K1 also clears the strip marks F of its edge slots
+    // K1 -> K2 overlap (both in one call): K1 publishes each finished tile as
+    // ready[t] = epoch (unique per call) and lets K2 launch early; K2's tasks
+    // wait for their tiles' flags instead of for K1's completion.  0: off.
+    unsigned long long epoch;
+    unsigned long long* ready;
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -171,6 +176,24 @@ __device__ __forceinline__ uint32_t nz16(uint4 v) {
 // slower (K3's blocks then hold shared memory the resolve / boundary blocks
 // need; 173 us with triggers at kernel entry, 148 with one in resolve).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// K2 side of the K1 -> K2 overlap: one lane waits for tile t's ready flag
+// (acquire), the warp synchronises behind it.
+__device__ __forceinline__ void wait_tile_ready(const Geom& g, size_t t) {
+    CCL_LOOP_GUARD(wr);
+    while (ld_acquire_u64(g.ready + t) != g.epoch) {
+        CCL_LOOP_TICK(wr);
+        __nanosleep(128);
+    }
+}
 // K3's barrier over its 256 compute threads (named barrier 1; the helper warp never joins)
 __device__ __forceinline__ void k3_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
@@ -990,6 +1013,13 @@ __device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ r
             }
         }
     }
+    if (g.epoch) {  // every output of the tile is written: publish it to the boundary analysis
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release_u64(g.ready + t, g.epoch);
+        }
+    }
 }
 
 
@@ -1410,7 +1440,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
                                                   int sub_log2 = 0) {
     __shared__ Word s_w[8][2][kWords];
     __shared__ int2 s_pairs[8][32 * kPairsPerLane];
-    pdl_wait();
+    if (!g.epoch) pdl_wait();  // else: each task waits for its own tiles' ready flags
     const int warp = threadIdx.x >> 5;
     // (task counts are < 2^31: <= 2 per 16 x 1024 tile; 32-bit index math)
     const unsigned task = blockIdx.x * 8u + unsigned(warp);
@@ -1424,6 +1454,15 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         const unsigned q2 = g.div_ty1.div(q);
         const int band = 1 + int(q - q2 * unsigned(g.tiles_y - 1));
         const int b = int(q2);
+        if (g.epoch) {  // the two tiles of the boundary and (8-conn corners) the upper tile's neighbours
+            const int lane = threadIdx.x & 31;
+            const size_t t_lo = tile_index(g, b, band, tx);
+            if (lane == 0) wait_tile_ready(g, t_lo);
+            if (lane == 1) wait_tile_ready(g, t_lo - g.tiles_x);
+            if (CONN == 8 && lane == 2 && tx > 0) wait_tile_ready(g, t_lo - g.tiles_x - 1);
+            if (CONN == 8 && lane == 3 && tx + 1 < g.tiles_x) wait_tile_ready(g, t_lo - g.tiles_x + 1);
+            __syncwarp();
+        }
         boundary_h<TY, CONN, (DBG & 4) != 0>(g, bits, R, E, G, b, band, tx, s_w[warp], s_pairs[warp],
                                              int(task & ((1u << sub_log2) - 1u)), sub_log2);
     } else if (task < nh_sub + unsigned(n_v)) {
@@ -1435,6 +1474,11 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         const unsigned groups = unsigned(g.tiles_y + v_bands<TY>() - 1) / v_bands<TY>();
         const int band0 = int(q - q2 * groups) * v_bands<TY>();
         const int b = int(q2);
+        if (g.epoch) {  // the tiles left and right of the edge in each of the bands
+            const int lane = threadIdx.x & 31, band = band0 + (lane >> 1);
+            if (lane < 2 * v_bands<TY>() && band < g.tiles_y) wait_tile_ready(g, tile_index(g, b, band, bx - (lane & 1)));
+            __syncwarp();
+        }
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
     }
     if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < nh_sub + unsigned(n_v)) {
@@ -1462,6 +1506,10 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     K1Smem<TY>& sm = *reinterpret_cast<K1Smem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned t = blockIdx.x;
+    // every K1 block is resident (persistent grid): the boundary analysis may
+    // be scheduled onto the SM slots K1's finished blocks free (its tasks wait
+    // on the per-tile ready flags)
+    if (g.epoch) pdl_launch_dependents();
     if (t >= ntiles) return;
     constexpr bool PF = VEC && k1_prefetches<TY>();
     // one register set: loaded with tile t before the loop, then refilled with
