@@ -218,22 +218,42 @@ def barrier(world):
 
 
 # ------------------------------------------------------------- cpu baseline
-def cpu_oracle_rate(imgs, conn, seconds):
-    """Oracle (as it stands, single-threaded C BFS) on whole images of the
-    workload until ~`seconds` of CPU work; returns (Mpx/s, images, labels0)."""
+def cpu_oracle_rate(imgs, conn, seconds, threads=1):
+    """Oracle (as it stands, C BFS) on whole images of the workload until
+    ~`seconds` of wall time; returns (Mpx/s, images, labels0, ms per image on
+    one core).  threads > 1 (C4, SURVEY.md §8(d) oracle plan): independent
+    frames labeled by a pool of host threads (the C call releases the GIL),
+    one frame per thread at a time."""
     import oracle
-    done_px, n, t0, first = 0, 0, time.perf_counter(), None
-    while True:
-        img = imgs[n % len(imgs)]
-        lab = oracle.label_bfs(img, conn)
-        if first is None:
-            first = lab
-        done_px += img.size
-        n += 1
+    t0 = time.perf_counter()
+    first = oracle.label_bfs(imgs[0], conn)
+    one_ms = (time.perf_counter() - t0) * 1e3
+    if threads <= 1:
+        done_px, n, t0 = 0, 0, time.perf_counter()
+        while True:
+            img = imgs[n % len(imgs)]
+            oracle.label_bfs(img, conn)
+            done_px += img.size
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= seconds or n >= 4 * len(imgs) and el > 1.0:
+                break
+        return done_px / el / 1e6, n, first, one_ms
+    import concurrent.futures as cf
+    n = max(threads, int(seconds * 1e3 / max(one_ms, 1e-3)) * threads)
+    n = min(n, 64 * threads)
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(lambda i: oracle.label_bfs(imgs[i % len(imgs)], conn), range(n)))
         el = time.perf_counter() - t0
-        if el >= seconds or n >= 4 * len(imgs) and el > 1.0:
-            break
-    return done_px / el / 1e6, n, first
+    return n * imgs[0].size / el / 1e6, n, first, one_ms
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # --------------------------------------------------------------------- main
@@ -398,7 +418,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": name, "connectivity": conn, "B": B, "H": H, "W": W, "gen": desc["gen"],
                    "px_per_rank": px_rank, "parallelism": f"dp{world} (independent images, no collective)",
                    "l2": f"flushed: {args.flush_mb} MiB memset before every timed step (outside events)",
-                   "tile": f"1024x{args.tile_rows or 16}"},
+                   "tile": f"1024x{args.tile_rows or ccl.default_tile_rows(B, H, W)}"},
         "per_gpu_mpx_s": round(px_rank / (ms / 1e3) / 1e6, 2),
         "wall_ms_per_step_incl_flush": round(1e3 * wall / K, 4),
         "step_ms": {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),
@@ -467,9 +487,13 @@ def run_ours(args, rank, world, local):
 
     # CPU oracle baseline (rank 0, N = 1 only) + parity of this run's output
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, n_imgs, lab0 = cpu_oracle_rate(imgs_np, conn, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": round(rate, 3), "unit": UNIT, "cores": 1, "cpu": cpu_model(), "kind": "oracle",
-                                "sample": f"{n_imgs} image(s) of {H}x{W} from the workload, C BFS, 1 thread"}
+        threads = host_cores() if name == "C4" else 1
+        rate, n_imgs, lab0, one_ms = cpu_oracle_rate(imgs_np, conn, args.cpu_seconds, threads)
+        line["cpu_baseline"] = {"value": round(rate, 3), "unit": UNIT, "cores": threads, "cpu": cpu_model(),
+                                "kind": "oracle", "single_core_ms_per_image": round(one_ms, 3),
+                                "sample": f"{n_imgs} image(s) of {H}x{W} from the workload, C BFS, "
+                                          + (f"thread pool of {threads} (one frame per thread)" if threads > 1
+                                             else "1 thread")}
         line["parity_vs_oracle"] = bool(np.array_equal(lab_gpu[0], lab0))
     else:
         line["cpu_baseline"] = None

@@ -97,9 +97,10 @@ ccl_status_t ccl_label_batched_async(const uint8_t* images, int64_t B, int64_t H
                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* As ccl_label_batched_async with an explicit tile height (rows per K1 thread
- * block: 8, 16 or 32; 0 = library default: 16, or 8 when 16-row tiles would
- * number fewer than 4 per SM of the current device, i.e. small images;
- * CCL_TILE_AUTO=0 in the environment pins the default to 16).  The tile width is fixed at 1024
+ * block: 8, 16 or 32; 0 = library default: the tallest of 32, 16, 8 whose
+ * tiles number at least 4 per SM of the current device -- 32 for C3 / C4 /
+ * C5-sized work, 8 for small images; CCL_TILE_AUTO=0 in the environment pins
+ * the default to 16).  The tile width is fixed at 1024
  * pixels (32 lanes x 32 px).  Output is identical for every tile config
  * ("config independence"); unsupported values -> CCL_ERR_CONFIG. */
 ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
@@ -206,6 +207,20 @@ ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t
                                        int64_t max_components, ccl_component_t* stats,
                                        int32_t* counts, void* workspace, size_t workspace_bytes,
                                        void* stream);
+/* As ccl_component_stats_async, and (relabel_out != NULL) also the compacted
+ * label map (SPEC.md:336 renumbering): relabel_out[p] = k for a pixel of the
+ * k-th component in label order (1..K_b per image, the record index + 1),
+ * 0 for background; device int32 [B][H][W], must not overlap the other
+ * buffers (CCL_ERR_ALIAS). */
+ccl_status_t ccl_component_stats_relabel_async(const int32_t* labels, int64_t B, int64_t H, int64_t W,
+                                               int64_t max_components, ccl_component_t* stats,
+                                               int32_t* counts, int32_t* relabel_out, void* workspace,
+                                               size_t workspace_bytes, void* stream);
+
+/* The tile height (8, 16 or 32) that tile_rows = 0 selects for this geometry
+ * on the current device (the rule of ccl_label_batched_cfg_async; the SM
+ * count is queried).  Host-only.  Returns -1 on invalid dimensions. */
+int ccl_default_tile_rows(int64_t B, int64_t H, int64_t W);
 
 /* Number of K2 boundary work items for the given geometry and tile height:
  * horizontal tile-edge segments (one warp each) and vertical tile-edge pixels

@@ -17,6 +17,9 @@ Contents
                         value" adjacency, every pixel labeled with its
                         component's 0-based minimum raster index.
 * ``label_3d``       -- 3D volumes (NEXT-4): C flood fill, 6- / 26-connectivity.
+* ``relabel_compact`` -- the 1..K renumbering of a canonical label map
+                        (SPEC.md:336): k for the k-th distinct label in
+                        increasing order, 0 for background.
 * ``component_stats`` -- per-component area, bounding box and coordinate sums
                         of a canonical label map, components in increasing
                         label order ("size
@@ -245,3 +248,17 @@ def component_stats(labels) -> dict:
     np.add.at(sum_y, inv, ys)
     return {"label": uniq, "area": area.astype(np.int64), "x_min": x_min, "y_min": y_min, "x_max": x_max,
             "y_max": y_max, "sum_x": sum_x, "sum_y": sum_y}
+
+
+def relabel_compact(labels) -> np.ndarray:
+    """The compact numbering of a label map [H,W] ("renumber
+    labels to 1..K", NEXT-3): pixel p gets k if labels[p] is the k-th
+    distinct nonzero label in increasing order, else 0.  Library primitive
+    only (np.unique's sorted inverse)."""
+    L = np.asarray(labels)
+    out = np.zeros(L.shape, dtype=np.int32)
+    fg = L != 0
+    if fg.any():
+        _, inv = np.unique(L[fg], return_inverse=True)
+        out[fg] = (inv + 1).astype(np.int32)
+    return out

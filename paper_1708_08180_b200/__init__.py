@@ -27,6 +27,7 @@ from ._binding import (  # noqa: F401
     SIGNATURES,
     Workspace,
     boundary_work_items,
+    default_tile_rows,
     label,
     raw,
     stage_fns,
@@ -35,5 +36,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "HostPipeline", "CCLError", "workspace_bytes", "boundary_work_items",
+__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "HostPipeline", "CCLError", "workspace_bytes", "boundary_work_items", "default_tile_rows",
            "stages", "stage_fns", "status_string", "raw"]

@@ -34,6 +34,7 @@ SIGNATURES = {
     "ccl_stage_local_merge": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _sz, _int, _vp]),
     "ccl_stage_boundary": (_int, [_i64, _i64, _i64, _int, _vp, _sz, _int, _vp]),
     "ccl_stage_link": (_int, [_i64, _i64, _i64, _int, _vp, _vp, _sz, _int, _vp]),
+    "ccl_default_tile_rows": (_int, [_i64, _i64, _i64]),
     "ccl_boundary_work_items": (_i64, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "ccl_host_scratch_bytes": (_sz, [_i64, _i64, _i64, _int]),
     "ccl_label_host_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
@@ -46,6 +47,7 @@ SIGNATURES = {
     "ccl_workspace_bytes_3d": (_sz, [_i64, _i64, _i64, _i64, _int]),
     "ccl_label_3d_async": (_int, [_vp, _i64, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
     "ccl_component_stats_async": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ccl_component_stats_relabel_async": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ccl_label_method_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _vp]),
 }
 
@@ -88,6 +90,14 @@ def status_string(status: int) -> str:
 
 def workspace_bytes(B: int, H: int, W: int, connectivity: int = 8) -> int:
     return int(_lib.ccl_workspace_bytes(B, H, W, connectivity))
+
+
+def default_tile_rows(B: int, H: int, W: int) -> int:
+    """The tile height tile_rows=0 selects for this geometry on the current device."""
+    ty = _lib.ccl_default_tile_rows(B, H, W)
+    if ty < 0:
+        raise ValueError("invalid geometry")
+    return int(ty)
 
 
 def boundary_work_items(B: int, H: int, W: int, tile_rows: int = 0):
@@ -290,12 +300,14 @@ def label_3d(volume, connectivity: int = 26, *, out=None, stream=None):
 STATS_FIELDS = ("label", "area", "x_min", "y_min", "x_max", "y_max", "sum_x", "sum_y")
 
 
-def component_stats(labels, max_components: int | None = None, stream=None):
+def component_stats(labels, max_components: int | None = None, stream=None, relabel: bool = False):
     """Per-component statistics of a label map from label() (NEXT-3,
-    ccl_component_stats_async): returns (counts [B] int32, dict field ->
-    tensor [B, max_components]) with the components of each image in
+    ccl_component_stats_relabel_async): returns (counts [B] int32, dict field
+    -> tensor [B, max_components]) with the components of each image in
     increasing label order (record k = component k+1 of the 1..K numbering).
-    Records beyond counts[b] (or beyond max_components) are not written."""
+    Records beyond counts[b] (or beyond max_components) are not written.
+    relabel=True also returns the compacted label map (1..K per image, 0 =
+    background) as a third element."""
     torch = _torch()
     if not isinstance(labels, torch.Tensor) or not labels.is_cuda or labels.dtype != torch.int32:
         raise TypeError("labels must be a CUDA int32 tensor")
@@ -309,15 +321,19 @@ def component_stats(labels, max_components: int | None = None, stream=None):
         counts = torch.zeros(max(B, 1), dtype=torch.int32, device=labels.device)
         ws_n = int(_lib.ccl_stats_workspace_bytes(B, H, W))
         ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=labels.device)
-        _check(_lib.ccl_component_stats_async(
+        rl = torch.empty(labels.shape, dtype=torch.int32, device=labels.device) if relabel else None
+        _check(_lib.ccl_component_stats_relabel_async(
             ctypes.c_void_p(labels.data_ptr()), B, H, W, int(max_components), ctypes.c_void_p(rec.data_ptr()),
-            ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws_n, _stream_ptr(s)),
-            "ccl_component_stats_async")
+            ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(rl.data_ptr() if relabel else 0),
+            ctypes.c_void_p(ws.data_ptr()), ws_n, _stream_ptr(s)),
+            "ccl_component_stats_relabel_async")
     i32 = rec.view(torch.int32)  # [B, max, 10]
     i64 = rec.view(torch.int64)  # [B, max, 5]
     out = {f: i32[..., k] for k, f in enumerate(STATS_FIELDS[:6])}
     out["sum_x"] = i64[..., 3]
     out["sum_y"] = i64[..., 4]
+    if relabel:
+        return counts[:B], {k: v[:B] for k, v in out.items()}, rl
     return counts[:B], {k: v[:B] for k, v in out.items()}
 
 

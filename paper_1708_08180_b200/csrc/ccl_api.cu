@@ -22,8 +22,7 @@ namespace {
 
 thread_local int g_last_cuda_error = 0;
 
-constexpr int kDefaultTileRows = 16;
-constexpr int64_t kSmallTilesPerSM = 4;  // below this many 16-row tiles per SM: 8-row tiles
+constexpr int64_t kSmallTilesPerSM = 4;  // default tile height: the tallest giving this many tiles per SM
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
@@ -56,8 +55,10 @@ int sm_count() {
 struct Plan {
     ccl::Geom g;
     int ty;
-    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, k1x_bytes, ready_bytes;
-    size_t total() const { return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + k1x_bytes + ready_bytes; }
+    size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, defer_bytes, ready_bytes;
+    size_t total() const {
+        return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + defer_bytes + ready_bytes;
+    }
 };
 
 ccl_status_t check_geometry(int64_t B, int64_t H, int64_t W, int conn) {
@@ -71,16 +72,21 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     ccl_status_t st = check_geometry(B, H, W, conn);
     if (st != CCL_OK) return st;
     if (tile_rows == 0) {
-        // Default tile height: 16 rows; 8 when 16-row tiles would not give
-        // the persistent K1 grid (SMs x 4-5 blocks) a tile per block --
-        // small images are latency-bound per tile (C1 512^2 noise 74 -> 56 us,
-        // C2 2048^2 noise 130 -> 102 us).  CCL_TILE_AUTO=0 disables the rule.
+        // Default tile height: the tallest of 32 / 16 / 8 rows that still gives
+        // the persistent K1 grid (SMs x 4-5 blocks) at least kSmallTilesPerSM
+        // tiles per SM.  Taller tiles halve the boundaries K2 unions and the
+        // tiles K3 walks (C3 8192^2 texture 113 -> 102.5 us at 32 rows); small
+        // images are latency-bound per tile (C1 512^2 noise 74 -> 56 us and C2
+        // 2048^2 noise 130 -> 102 us at 8 rows).  CCL_TILE_AUTO=0 pins it to 16.
         static const bool autoty = [] {
             const char* v = std::getenv("CCL_TILE_AUTO");
             return !(v && v[0] == '0');
         }();
-        const int64_t tiles16 = B * ((W + ccl::kTileW - 1) / ccl::kTileW) * ((H + 15) / 16);
-        tile_rows = (autoty && tiles16 < kSmallTilesPerSM * sm_count()) ? 8 : kDefaultTileRows;
+        const int64_t tx = (W + ccl::kTileW - 1) / ccl::kTileW, need = kSmallTilesPerSM * sm_count();
+        if (!autoty) tile_rows = 16;
+        else if (B * tx * ((H + 31) / 32) >= need) tile_rows = 32;
+        else if (B * tx * ((H + 15) / 16) >= need) tile_rows = 16;
+        else tile_rows = 8;
     }
     if (tile_rows != 8 && tile_rows != 16 && tile_rows != 32) return CCL_ERR_CONFIG;
     if (B > INT32_MAX) return CCL_ERR_DIMS;
@@ -105,6 +111,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.strip = 0;
     p.g.epoch = 0;
     p.g.ready = nullptr;
+    p.g.defer = nullptr;
     p.g.ntiles = unsigned(int64_t(B) * p.g.tiles_x * p.g.tiles_y);
     // edge slots (the boundary analysis' union-find nodes, 8 B each) and their
     // resolved labels in strip mode (4 B each): edge_slots(TY) per tile, sized
@@ -126,10 +133,7 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     // makes (tile_rows = 8)
     p.edge_bytes = align_up(tiles8 * ccl::kEdgeCap * sizeof(int32_t));
     p.ready_bytes = align_up(tiles8 * sizeof(uint64_t));  // per-tile ready flags (K1 -> K2 overlap)
-    // K1 scratch slots for tiles over the shared-memory run capacity (one per
-    // K1 block; tile_rows = 8 never overflows), sized for the larger need
-    p.k1x_bytes = align_up(std::max(std::min(tiles16, size_t(ccl::k1x_slots<16>())) * ccl::k1x_slot_bytes<16>(),
-                                    std::min(tiles32, size_t(ccl::k1x_slots<32>())) * ccl::k1x_slot_bytes<32>()));
+    p.defer_bytes = align_up(tiles8 * sizeof(int32_t));   // K1's lists of run-dense tiles
     return CCL_OK;
 }
 
@@ -304,9 +308,7 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     if (ntiles == 0) return cudaSuccess;
     const size_t smem = smem_bytes<TY>();
     // persistent K1/K3: one wave of resident blocks walks all tiles
-    const unsigned grid1 = unsigned(std::min<long long>(
-        std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)), ccl::k1x_slots<TY>()));
-    void* k1x = reinterpret_cast<char*>(F) + p.F_bytes;
+    const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
     const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
     const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
@@ -321,9 +323,10 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
         g.epoch = next_epoch();
         g.ready = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + p.total() - p.ready_bytes);
     }
+    g.defer = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p.total() - p.ready_bytes - p.defer_bytes);
     if (stages & kK1) {
         ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::k1_threads<TY>(), smem_bytes_k1<TY>(), s>>>(
-            img, g, bits, G, runs, E, F, k1x, unsigned(ntiles));
+            img, g, bits, G, runs, E, F, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
@@ -680,6 +683,14 @@ size_t ccl_stats_workspace_bytes(int64_t B, int64_t H, int64_t W) {
 ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t H, int64_t W,
                                        int64_t max_components, ccl_component_t* stats, int32_t* counts,
                                        void* workspace, size_t workspace_bytes, void* stream) {
+    return ccl_component_stats_relabel_async(labels, B, H, W, max_components, stats, counts, nullptr, workspace,
+                                             workspace_bytes, stream);
+}
+
+ccl_status_t ccl_component_stats_relabel_async(const int32_t* labels, int64_t B, int64_t H, int64_t W,
+                                               int64_t max_components, ccl_component_t* stats, int32_t* counts,
+                                               int32_t* relabel_out, void* workspace, size_t workspace_bytes,
+                                               void* stream) {
     ccl_status_t st = check_geometry(B, H, W, 8);
     if (st != CCL_OK) return st;
     if (max_components < 1 || B > 65535) return CCL_ERR_DIMS;
@@ -692,6 +703,10 @@ ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t
         overlaps(stats, ns, workspace, workspace_bytes) || overlaps(counts, size_t(B) * 4, stats, ns) ||
         overlaps(counts, size_t(B) * 4, workspace, workspace_bytes) || overlaps(counts, size_t(B) * 4, labels, nl))
         return CCL_ERR_ALIAS;
+    if (relabel_out && (overlaps(relabel_out, nl, labels, nl) || overlaps(relabel_out, nl, stats, ns) ||
+                        overlaps(relabel_out, nl, workspace, workspace_bytes) ||
+                        overlaps(relabel_out, nl, counts, size_t(B) * 4)))
+        return CCL_ERR_ALIAS;
     namespace cs = ccl::stats;
     const int nchunks = int((npx + cs::kChunk - 1) / cs::kChunk);
     int32_t* M = static_cast<int32_t*>(workspace);
@@ -703,7 +718,8 @@ ccl_status_t ccl_component_stats_async(const int32_t* labels, int64_t B, int64_t
     cs::k_stats_rank<<<gc, cs::kT, 0, s>>>(labels, npx, int(W), nchunks, cnt, M, stats, max_components);
     const unsigned ablocks = unsigned(std::max<long long>(1, std::min<long long>((npx + 16 * cs::kT - 1) / (16 * cs::kT),
                                                                                    std::max<long long>(1, (long long)sm_count() * 8 / B))));
-    cs::k_stats_accum<<<dim3(ablocks, unsigned(B)), cs::kT, 0, s>>>(labels, npx, int(W), M, stats, max_components);
+    cs::k_stats_accum<<<dim3(ablocks, unsigned(B)), cs::kT, 0, s>>>(labels, npx, int(W), M, stats, max_components,
+                                                                  relabel_out);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CCL_OK : cuda_fail(e);
 }
@@ -739,6 +755,12 @@ ccl_status_t ccl_stage_link(int64_t B, int64_t H, int64_t W, int connectivity, i
                             void* workspace, size_t workspace_bytes, int tile_rows, void* stream) {
     return stage(nullptr, B, H, W, connectivity, labels_out, workspace, workspace_bytes, tile_rows,
                  kK3, stream);
+}
+
+int ccl_default_tile_rows(int64_t B, int64_t H, int64_t W) {
+    Plan p;
+    if (make_plan(B, H, W, 4, 0, p) != CCL_OK) return -1;
+    return p.ty;
 }
 
 int64_t ccl_boundary_work_items(int64_t B, int64_t H, int64_t W, int tile_rows,

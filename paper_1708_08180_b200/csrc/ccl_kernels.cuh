@@ -30,6 +30,7 @@
 //    ~ 1 B (image) + 4 B (labels) + 1/4 B (mask) + edge entries.
 #pragma once
 #include <cassert>
+#include <cstdio>
 #include <climits>
 #include <cstdint>
 #include <cuda.h>  // CUtensorMap (TMA descriptors; encoded on the host in ccl_api.cu)
@@ -63,6 +64,40 @@ template <int TY>
 __host__ __device__ constexpr int k1_threads() { return TY > 16 ? CCL_K1_T32 : 256; }
 template <int TY>
 __host__ __device__ constexpr int k1_warps() { return k1_threads<TY>() / 32; }
+
+// Run lists of a tile live in shared memory up to k1_cap runs (natural
+// images: a few hundred; i.i.d. noise at density 1/2: ~4096 per 16 rows),
+// which keeps the block at 45 KB -- with one prefetch register set (44
+// registers) 5 blocks (40 warps) per SM; measured: 4 blocks 46.8 us, 5 blocks
+// 43.6 us on C3 texture.  A tile with more runs (noise in 32-row tiles,
+// period-2 stripes, checkerboards: up to TY*512) is labelled in maximal row
+// ranges that fit (k1_range), whose boundaries are unioned like tile
+// boundaries.
+#ifndef CCL_K1_CAP16
+#define CCL_K1_CAP16 4576
+#endif
+#ifndef CCL_K1_BLOCKS
+#define CCL_K1_BLOCKS 5
+#endif
+#ifndef CCL_K1_BLOCKS32
+#define CCL_K1_BLOCKS32 5  // 32-row tiles: 5 blocks per SM (48 registers; 3456 runs in shared memory)
+#endif
+__host__ __device__ constexpr int k1_cap32() {
+    // 16 KB of row words; 512 threads: 11776 runs (110 KB, 2 blocks per SM);
+    // 256 threads: 4800 runs at 4 blocks per SM (54 KB), 3456 at 5 (44 KB)
+    return CCL_K1_T32 == 512 ? 11776 : (CCL_K1_BLOCKS32 == 4 ? 4800 : 3456);
+}
+__host__ __device__ constexpr int k1_cap_n(int TY) {
+    return TY * kTileW / 2 < (TY > 16 ? k1_cap32() : CCL_K1_CAP16) ? TY * kTileW / 2
+                                                                   : (TY > 16 ? k1_cap32() : CCL_K1_CAP16);
+}
+template <int TY>
+__host__ __device__ constexpr int k1_cap() { return k1_cap_n(TY); }
+// most row ranges a tile can need: every range but the last holds more than
+// k1_cap - 512 runs (else one more row would have fitted)
+__host__ __device__ constexpr int k1_max_ranges(int TY) {
+    return TY * kTileW / 2 <= k1_cap_n(TY) ? 1 : 1 + (TY * kTileW / 2) / (k1_cap_n(TY) - kTileW / 2 + 1);
+}
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
 
@@ -100,6 +135,7 @@ struct Geom {
     // wait for their tiles' flags instead of for K1's completion.  0: off.
     unsigned long long epoch;
     unsigned long long* ready;
+    int32_t* defer;    // K1's per-block lists of run-dense tiles (ntiles ints)
 };
 
 // One 32-px mask word with its row-run description (one 128-bit smem load).
@@ -133,7 +169,11 @@ __host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; 
 // share a line or sector (a layout with one tile per 8-byte step measured
 // K2 25 -> 37 us: atomics and pointer-jumping stores of different tiles on
 // one line), and K1 writes each tile's entries as whole 32-byte sectors.
-__host__ __device__ constexpr int edge_slots(int TY) { return (2 * (kTileW / 2) + 2 * TY + 15) / 16 * 16; }
+// (capacity: every row next to a tile edge or a range boundary can carry 512
+// edge roots, the columns 2 * TY, each range pads to a whole sector)
+__host__ __device__ constexpr int edge_slots(int TY) {
+    return (2 * k1_max_ranges(TY) * (kTileW / 2) + 2 * TY + 4 * k1_max_ranges(TY) + 15) / 16 * 16;
+}
 __host__ __device__ inline unsigned edge_slot(unsigned ntiles, int i, unsigned t) {
     return ((unsigned(i) >> 4) * ntiles + t) * 16u + (unsigned(i) & 15u);
 }
@@ -441,698 +481,6 @@ __device__ __forceinline__ TileId decode_tile(const Geom& g, unsigned t) {
     return id;
 }
 
-// =========================================================== K1: local merge
-// The tile's foreground is first turned into compact run lists (one entry per
-// row run, in raster order of the run starts) so every later step -- local UF,
-// flatten, edge output, per-run records -- runs one thread per run with all
-// lanes busy, instead of looping over the set bits of each lane's mask word.
-//
-// Coarse labeling (Alg. 1 l.9-24): the row scan + row-column unification in
-// the row direction is exact here -- every pixel's provisional label is its
-// run, the lowest equivalent label of its row segment (PAPER.md:230).
-// Local UF (Alg. 1 l.25-33): each run of row r >= 1 finds the runs of row r-1
-// it touches in O(1) from the masks (they are a contiguous index range of the
-// sorted upper run list) and min-unions with each (8-conn widens the contact
-// interval by one pixel on both sides: the NW / NE diagonals, reading R2/R10).
-// Persistent: each block walks tiles t = blockIdx.x, +gridDim.x, ...; the
-// 128-bit image loads of the NEXT tile are issued into registers before the
-// current tile is processed, so HBM reads overlap the shared-memory work.
-
-// One 32-px mask word of a K1 tile row.
-struct __align__(16) WordE {
-    uint32_t m;    // foreground mask
-    uint32_t s;    // run-start mask (tile-local runs)
-    uint32_t e;    // run-end mask
-    int32_t pad;   // number of run starts in the row before this word
-};
-
-// Run lists of a tile live in shared memory up to k1_cap runs (natural
-// images: a few hundred; i.i.d. noise at density 1/2: ~4096), which keeps the
-// block at 45 KB -- with one prefetch register set (44 registers) 5 blocks
-// (40 warps) per SM; measured: 4 blocks 46.8 us, 5 blocks 43.6 us on C3
-// texture (a cap of 4096 also allowed 5 blocks but sent half the noise tiles
-// to the scratch path).  A tile with more runs (period-2 stripes,
-// checkerboards: up to TY*512) keeps them in the block's slot of a global
-// scratch area instead (same code, L2-resident).
-#ifndef CCL_K1_CAP16
-#define CCL_K1_CAP16 4576
-#endif
-#ifndef CCL_K1_UF2
-#define CCL_K1_UF2 0  // two-step local UF (up-link forest, then the remaining pairs)
-#endif
-#ifndef CCL_K1_V8
-#define CCL_K1_V8 1  // lane owns 32 contiguous pixels (256-bit loads), else 2 x 16 B + shuffles
-#endif
-#ifndef CCL_K1_RUNLOOP
-#define CCL_K1_RUNLOOP 0  // run lists: 0 two loops, 1 one joint loop, 2 peeled (<= 2 without a loop)
-#endif
-#ifndef CCL_K1_DENSE
-#define CCL_K1_DENSE (1 << 30)  // tiles with more runs take the random-priority local UF (r02: slower on noise, off)
-#endif
-#ifndef CCL_K1_UFDEDUP
-#define CCL_K1_UFDEDUP 0  // union each adjacency pair once (not from both of its runs)
-#endif
-#ifndef CCL_K1_BLOCKS
-#define CCL_K1_BLOCKS 5
-#endif
-__host__ __device__ constexpr int k1_cap32() { return CCL_K1_T32 == 512 ? 11776 : 3456; }
-template <int TY>
-__host__ __device__ constexpr int k1_cap() {
-    // TY = 32: 16 KB of row words; 512 threads: 11776 runs (110 KB, 2 blocks
-    // per SM); 256 threads: 3456 runs keep the block at 44 KB (5 per SM)
-    return TY * kTileW / 2 < (TY > 16 ? k1_cap32() : CCL_K1_CAP16) ? TY * kTileW / 2
-                                                                   : (TY > 16 ? k1_cap32() : CCL_K1_CAP16);
-}
-template <int TY>
-__host__ __device__ constexpr int k1_min_blocks() { return (TY > 16 && CCL_K1_T32 == 512) ? 2 : CCL_K1_BLOCKS; }
-template <int TY>
-__host__ __device__ constexpr size_t k1x_slot_bytes() { return (size_t(TY) * (kTileW / 2) + 8) * 8; }
-template <int TY>
-__host__ __device__ constexpr int k1x_slots() { return TY > 16 ? 768 : 1024; }  // = max K1 grid (148 SMs x 5)
-
-template <int TY>
-struct K1Smem {
-    WordE wd[TY][kWords];
-    uint16_t rs[k1_cap<TY>() + 8];  // run k: start x | row << 10; rs[total] = sentinel row 63
-    uint16_t re[k1_cap<TY>() + 8];  // run k: end x
-    // parent over tile run ids (min-root forest).  After the flatten, a root
-    // whose component touches a tile edge carries bit 31 and (1 + its
-    // edge-list index) << 16; the low 16 bits are always the parent id.
-    int32_t P[k1_cap<TY>()];
-    int32_t ecount;                // edge-list length
-    int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
-    int32_t rcnt[TY];              // runs per row
-    int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
-};
-
-// find / merge of §2.1.3 (PAPER.md:311-313) over tile run ids.
-#ifdef CCL_STATS
-__device__ unsigned long long g_stat_k1_unions = 0, g_stat_k1_steps = 0, g_stat_k1_hops = 0;
-#endif
-__device__ __forceinline__ int find_r(int32_t* P, int a) {
-    volatile int32_t* V = P;
-    int p = V[a];
-    CCL_LOOP_GUARD(fr);
-    while (p != a) {
-        CCL_LOOP_TICK(fr);
-        CCL_STAT(g_stat_k1_hops);
-        const int gp = V[p];
-        if (gp != p) V[a] = gp;  // path halving: re-point at an ancestor
-        a = p;
-        p = gp;
-    }
-    return a;
-}
-
-// read-only find during the flatten: edge tags may be landing on roots, so
-// only the low 16 bits (the parent id) are followed
-__device__ __forceinline__ int find_r_ro(const int32_t* P, int a) {
-    const volatile int32_t* V = P;
-    int p = V[a] & 0xFFFF;
-    CCL_LOOP_GUARD(fro);
-    while (p != a) {
-        CCL_LOOP_TICK(fro);
-        a = p;
-        p = V[a] & 0xFFFF;
-    }
-    return a;
-}
-
-// Lock-free minimum-root union (reading R11): the larger root is re-pointed at
-// the smaller with atomicMin; if someone else re-linked it first, retry with
-// the value it was linked to.
-__device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
-    CCL_STAT(g_stat_k1_unions);
-    while (true) {
-        CCL_STAT(g_stat_k1_steps);
-        a = find_r(P, a);
-        b = find_r(P, b);
-        if (a == b) return;
-        if (a < b) { int t = a; a = b; b = t; }
-        const int old = atomicMin(&P[a], b);
-        if (old == a) return;
-        a = old;
-    }
-}
-
-// K1's union call; profiling variants (DBG bit 8: skipped, bit 16: one
-// atomicMin without finds -- timing only, the labels are then wrong).
-template <int DBG>
-__device__ __forceinline__ void k1_union(int32_t* P, int a, int b) {
-    if (DBG & 8) return;
-    if (DBG & 16) {
-        atomicMin(&P[a], b);
-        return;
-    }
-    union_r(P, a, b);
-}
-
-// Run-dense tiles (i.i.d. noise: ~4096 runs per 16-row tile, one giant
-// component): min-id linking strings the roots of a row into chains as long
-// as the row's run count (a zigzag between two rows links run j+1 under j for
-// every j at once), and the finds then walk them -- the union phase was 78 %
-// of a noise tile.  Here the unions link by a random priority instead (a
-// fixed bijective hash of the run id, ties impossible), which keeps expected
-// tree depth logarithmic; the component minimum (the canonical root, reading
-// R3) is then found with one atomic per run and every run is re-pointed at it,
-// so the flatten / edge / record steps see the same min-rooted forest as on
-// the sparse path.
-__device__ __forceinline__ uint32_t k1_prio(int x) {
-    return ((uint32_t(x) * 0x9E3779B1u) & 0xFFFF0000u) | uint32_t(x);  // hash high, id low: a total order
-}
-
-__device__ __forceinline__ void union_prio(int32_t* P, int a, int b) {
-    CCL_LOOP_GUARD(up);
-    while (true) {
-        CCL_LOOP_TICK(up);
-        a = find_r(P, a);
-        b = find_r(P, b);
-        if (a == b) return;
-        if (k1_prio(a) > k1_prio(b)) { const int t = a; a = b; b = t; }
-        if (atomicCAS(&P[a], a, b) == a) return;  // a stayed a root: linked under b
-    }
-}
-
-// Profiling builds only (DBG bit 2): per-tile phase timestamps.
-__device__ unsigned long long* g_k1_stamps = nullptr;
-__device__ unsigned long long* g_k3_stamps = nullptr;
-__device__ unsigned long long* g_k2_stamps = nullptr;  // per K2 task: start, end (globaltimer ns)
-__device__ unsigned long long* g_k2_phase = nullptr;   // per horizontal K2 task: masks in, records in, 1st batch done
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void k1_stamp(unsigned t, int k) {
-    if (g_k1_stamps) g_k1_stamps[size_t(t) * 8 + k] = clock64();
-}
-__device__ __forceinline__ void k3_stamp(unsigned t, int k) {
-    if (g_k3_stamps) g_k3_stamps[size_t(t) * 8 + k] = clock64();
-}
-
-template <int TY>
-struct ImgRegs {
-    uint4 v[(TY + k1_warps<TY>() - 1) / k1_warps<TY>()][2];  // row i of the warp: bytes 32*lane .. 32*lane + 31
-};
-
-template <int TY>
-__host__ __device__ constexpr bool k1_prefetches() { return (TY + k1_warps<TY>() - 1) / k1_warps<TY>() <= 2; }
-
-// One lane's 32 contiguous pixels of a tile row: one 256-bit load when the
-// row is 32-byte aligned (W % 32 == 0 and an aligned image), else two 128-bit
-// loads (the row is 16-byte aligned on the vector path); pixels at or beyond
-// W read as background.  A warp instruction covers the whole 1024-px row.
-__device__ __forceinline__ void ld_px32(const uint8_t* p, int avail, bool v8, uint4& a, uint4& b) {
-    a = b = make_uint4(0, 0, 0, 0);
-    if (avail >= 32 && v8) {
-        asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                     : "l"(p));
-    } else {
-        if (avail >= 16) a = ld_stream_u4(p);
-        if (avail >= 32) b = ld_stream_u4(p + 16);
-    }
-}
-
-template <int TY>
-__device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, unsigned t, int warp,
-                                            int lane, bool v8, ImgRegs<TY>& pf) {
-    const TileId id = decode_tile<TY>(g, t);
-    const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
-#pragma unroll
-    for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
-        const int y = (warp + i * k1_warps<TY>() < TY) ? id.y0 + warp + i * k1_warps<TY>() : g.H;
-        pf.v[i][0] = pf.v[i][1] = make_uint4(0, 0, 0, 0);
-#if CCL_K1_V8
-        const int x = id.x0 + 32 * lane;
-        if (y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, pf.v[i][0], pf.v[i][1]);
-#else
-        if (y < g.H) {
-            const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
-            if (id.x0 + 16 * lane < g.W) pf.v[i][0] = ld_stream_u4(row + 16 * lane);
-            if (id.x0 + 512 + 16 * lane < g.W) pf.v[i][1] = ld_stream_u4(row + 512 + 16 * lane);
-        }
-#endif
-    }
-}
-
-// Row r's mask word for this lane -> start / end masks, row-local run offsets.
-template <int TY>
-__device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uint32_t m) {
-    uint32_t pm = __shfl_up_sync(kFull, m, 1), nm = __shfl_down_sync(kFull, m, 1);
-    if (lane == 0) pm = 0;
-    if (lane == 31) nm = 0;
-    const uint32_t s = m & ~((m << 1) | (pm >> 31));
-    const uint32_t e = m & ~((m >> 1) | (nm << 31));
-    const int n = __popc(s);
-    int incl = n;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
-    }
-    sm.wd[r][lane] = WordE{m, s, e, incl - n};
-    if (lane == 31) sm.rcnt[r] = incl;
-}
-
-// K1 from the run lists on: rs / re / P are the block's shared arrays or, for
-// a tile over k1_cap runs, its global scratch slot.
-template <int TY, int CONN, int DBG>
-__device__ __forceinline__ void k1_runs(K1Smem<TY>& sm, uint16_t* __restrict__ rs, uint16_t* __restrict__ re,
-                                        int32_t* P, const Geom& g, unsigned t, const TileId& id, int v,
-                                        int total, uint64_t* G, uint32_t* R, int32_t* E, int32_t* F, int warp,
-                                        int lane) {
-    const int tid = threadIdx.x;
-    // run lists: rs / re in raster order of the starts (one loop over the
-    // word's starts and ends together: starts and ends alternate, so a word
-    // holds at most one more of either)
-    {
-        for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
-            const int r = warp + i * k1_warps<TY>();
-            if (r >= TY) break;  // warp-uniform
-            const int rb = __shfl_sync(kFull, v, r > 0 ? r - 1 : 0) * (r > 0);
-            const WordE w = sm.wd[r][lane];
-            sm.wd[r][lane].pad = rb + w.pad;  // from here on: tile run id of the word's first start
-            const int xb = lane << 5;
-            int ks = rb + w.pad;
-            int ke = ks - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
-            uint32_t sb = w.s, eb = w.e;
-#if CCL_K1_RUNLOOP == 2
-            // peeled: a word's first two starts / ends without a loop (97 % of
-            // texture words have <= 1 start); only denser words loop
-            {
-                const int cs = __popc(sb), ce = __popc(eb);
-                if (cs >= 1) rs[ks] = uint16_t((xb + __ffs(sb) - 1) | (r << 10));
-                sb &= sb - 1;
-                if (cs >= 2) rs[ks + 1] = uint16_t((xb + __ffs(sb) - 1) | (r << 10));
-                sb &= sb - 1;
-                if (ce >= 1) re[ke] = uint16_t(xb + __ffs(eb) - 1);
-                eb &= eb - 1;
-                if (ce >= 2) re[ke + 1] = uint16_t(xb + __ffs(eb) - 1);
-                eb &= eb - 1;
-                ks += 2;
-                ke += 2;
-                while (sb) {
-                    const int bit = __ffs(sb) - 1;
-                    sb &= sb - 1;
-                    rs[ks++] = uint16_t((xb + bit) | (r << 10));
-                }
-                while (eb) {
-                    const int bit = __ffs(eb) - 1;
-                    eb &= eb - 1;
-                    re[ke++] = uint16_t(xb + bit);
-                }
-            }
-#elif CCL_K1_RUNLOOP == 1
-            while (sb | eb) {
-                if (sb) {
-                    const int bit = __ffs(sb) - 1;
-                    sb &= sb - 1;
-                    rs[ks] = uint16_t((xb + bit) | (r << 10));
-#if !CCL_K1_UF2
-                    P[ks] = ks;
-#endif
-                    ++ks;
-                }
-                if (eb) {
-                    const int bit = __ffs(eb) - 1;
-                    eb &= eb - 1;
-                    re[ke++] = uint16_t(xb + bit);
-                }
-            }
-#else
-            while (sb) {
-                const int bit = __ffs(sb) - 1;
-                sb &= sb - 1;
-                rs[ks] = uint16_t((xb + bit) | (r << 10));
-#if !CCL_K1_UF2
-                P[ks] = ks;
-#endif
-                ++ks;
-            }
-            while (eb) {
-                const int bit = __ffs(eb) - 1;
-                eb &= eb - 1;
-                re[ke++] = uint16_t(xb + bit);
-            }
-#endif
-        }
-        if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
-#if CCL_K1_RUNLOOP == 2 && !CCL_K1_UF2
-        // P[k] = k for every run, four entries per 128-bit store
-        for (int k = 4 * tid; k < total; k += 4 * k1_threads<TY>())
-            *reinterpret_cast<int4*>(P + k) = make_int4(k, k + 1, k + 2, k + 3);
-#endif
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
-    if (DBG & 1) {
-        __syncthreads();
-        return;
-    }
-
-    // local UF.  The adjacencies between two rows form a monotone staircase of
-    // run pairs; every pair is (k, first upper neighbour of k) or (first lower
-    // neighbour of j, j) -- if j is the 2nd+ upper neighbour of k, j starts
-    // right of k's start, so it cannot reach k-1.  Each run therefore does at
-    // most two unions, found in O(1) from the masks: no fan-in serialisation.
-    constexpr int D = CONN == 8 ? 1 : 0;
-#if CCL_K1_UF2
-    // Two steps, every adjacency pair exactly once:
-    //  U1  P[k] = k's first upper neighbour (or k): a forest of up-links made
-    //      with plain stores -- each tree's root is its minimum run id (all
-    //      its other runs lie in lower rows) and no two threads touch one
-    //      entry, so no atomics and no retries;
-    //  U2  the remaining pairs (first lower neighbour jd of k, k) for which k
-    //      is NOT jd's first upper neighbour (i.e. run k-1 of the same row
-    //      also touches jd) are min-root unions on that forest.
-    // (Concurrent unions of all pairs at once built up-chains through every
-    // row and retried under contention: K1's union phase was 34 % of a
-    // texture tile and 78 % of a noise tile.)
-#pragma unroll 1
-    for (int k = tid; k < total; k += k1_threads<TY>()) {
-        const int rsk = rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
-        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        int parent = k;
-        if (r > 0) {
-            const WordE uu = sm.wd[r - 1][p >> 5];
-            const uint32_t below = (1u << (p & 31)) - 1u;
-            const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
-            const int rsu = rs[ju];
-            if ((rsu >> 10) == r - 1 && (rsu & 1023) <= q) parent = ju;
-        }
-        if (DBG & 8) parent = k;
-        P[k] = parent;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int k = tid; k < total; k += k1_threads<TY>()) {
-        const int rsk = rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
-        if (r + 1 >= TY || k == 0) continue;
-        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        const WordE ud = sm.wd[r + 1][p >> 5];
-        const uint32_t below = (1u << (p & 31)) - 1u;
-        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
-        const int rsd = rs[jd], rsp = rs[k - 1], ep = re[k - 1];
-        // jd touches k, and run k-1 (same row) touches jd too: k is a 2nd+ upper neighbour of jd
-        if ((rsd >> 10) == r + 1 && (rsd & 1023) <= q && (rsp >> 10) == r && ep + D >= (rsd & 1023))
-            k1_union<DBG>(P, jd, k);
-    }
-#else
-    if (total > CCL_K1_DENSE) {
-#pragma unroll 1
-        for (int k = tid; k < total; k += k1_threads<TY>()) {
-            const int rsk = rs[k];
-            const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
-            const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-            const WordE uu = sm.wd[r > 0 ? r - 1 : 0][p >> 5];
-            const WordE ud = sm.wd[r + 1 < TY ? r + 1 : TY - 1][p >> 5];
-            const uint32_t below = (1u << (p & 31)) - 1u;
-            const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
-            const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
-            const int rsu = rs[ju], rsd = rs[jd];
-            if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) union_prio(P, k, ju);
-            if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) union_prio(P, jd, k);
-        }
-        __syncthreads();
-        // component minimum at the root: high 16 bits = 0xFFFF - min member
-        // (unsigned atomicMax; the low 16 bits of a root entry stay its id);
-        // every other run is pointed straight at its root
-#pragma unroll 1
-        for (int k = tid; k < total; k += k1_threads<TY>()) {
-            const int r = find_r_ro(P, k);
-            if (r != k) P[k] = r;
-            atomicMax(reinterpret_cast<unsigned*>(P + r), ((0xFFFFu - uint32_t(k)) << 16) | uint32_t(r));
-        }
-        __syncthreads();
-        // each root r hands its component to the minimum m: P[r] = m, P[m] = m
-#pragma unroll 1
-        for (int k = tid; k < total; k += k1_threads<TY>()) {
-            const uint32_t v = uint32_t(P[k]);
-            if (v >> 16) {  // a root (only roots carry the packed minimum; P[m] = m below clears it)
-                const int m = int(0xFFFFu - (v >> 16));
-                P[k] = m;
-                if (m != k) P[m] = m;
-            }
-        }
-        __syncthreads();
-        // every run one hop further: its root's entry now names the minimum
-#pragma unroll 1
-        for (int k = tid; k < total; k += k1_threads<TY>()) {
-            const int pk = P[k];
-            if (pk != k) P[k] = P[pk];
-        }
-    } else {
-#pragma unroll 1
-    for (int k = tid; k < total; k += k1_threads<TY>()) {
-        const int rsk = rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
-        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        // first runs of rows r-1 and r+1 touching [p, q] (both searches are
-        // issued before either union: the phase is bound by this chain)
-        const WordE uu = sm.wd[r > 0 ? r - 1 : 0][p >> 5];
-        const WordE ud = sm.wd[r + 1 < TY ? r + 1 : TY - 1][p >> 5];
-        const uint32_t below = (1u << (p & 31)) - 1u;
-        const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
-        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
-        const int rsu = rs[ju], rsd = rs[jd];  // may be another row's run or the sentinel
-#if CCL_K1_UFDEDUP
-        // (jd, k) is also jd's own (jd, first upper neighbour) pair unless run
-        // k-1 of this row touches jd as well: union each pair once
-        const int rsp = k > 0 ? rs[k - 1] : 0, ep = k > 0 ? re[k - 1] : 0;
-        if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
-        if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q && k > 0 && (rsp >> 10) == r &&
-            ep + D >= (rsd & 1023))
-            k1_union<DBG>(P, jd, k);
-#else
-        if (r > 0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
-        if (r + 1 < TY && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) k1_union<DBG>(P, jd, k);
-#endif
-    }
-    }
-#endif
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
-    // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
-    // index conversion): every run points at its root; the first run to find
-    // that its root's component touches a tile edge (top / bottom row run,
-    // left / right column pixel) claims the root (bit 31), takes the next
-    // edge index i of the tile and tags the root with 1 + i (claim order: any
-    // bijection works, the labels do not depend on it); the root becomes
-    // edge slot i * ntiles + t with entry (global raster index << 32) | slot.
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
-    const int W = g.W, x0 = id.x0, y0 = id.y0;
-    // rows that border another tile (or, in strip mode, another strip)
-    const int last_row = min(TY, g.H - y0) - 1;
-    const bool top = y0 > 0 || g.force_top;
-    const bool bottom = y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
-    const bool left = x0 > 0, right = x0 + kTileW < W;
-    int32_t* Eh = E + size_t(t) * kEdgeCap;
-#pragma unroll 1
-    for (int k = tid; k < total; k += k1_threads<TY>()) {
-        const int root = find_r_ro(P, k);
-        if (root != k) P[k] = root;  // an ancestor: concurrent finds stay valid
-        const int rsk = rs[k];
-        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
-        const bool hrow = (r == 0 && top) || (r == last_row && bottom);
-        const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
-        if (hrow || lc || rc) {
-            if (!(atomicOr(&P[root], int(0x80000000u)) & int(0x80000000u))) {
-                const int idx = atomicAdd(&sm.ecount, 1);
-                P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
-            }
-            if (lc) sm.lc[r] = k;  // the column pixel's run (its root's slot after the claims)
-            if (rc) sm.rc[r] = k;
-        }
-    }
-    if (DBG & 2) {
-        __syncthreads();
-        __syncthreads();
-        return;
-    }
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
-    // edge brief: header, column-root slots; per-run records for K3 / K2
-    if (tid == 0) {
-        st_keep(Eh, sm.ecount);
-        st_keep(Eh + 1, sm.rbase[last_row]);  // first run of the last valid row
-    }
-    if (tid < 2 * TY) {
-        const int k = tid < TY ? sm.lc[tid] : sm.rc[tid - TY];
-        int slot = -1;
-        if (k >= 0) slot = int(edge_slot(g.ntiles, ((P[P[k] & 0xFFFF] >> 16) & 0x7FFF) - 1, t));
-        st_keep(Eh + (tid < TY ? kEdgeLC + tid : kEdgeRC + tid - TY), slot);
-    }
-    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
-    const int rb_last = sm.rbase[last_row];
-    const int ne = sm.ecount;  // (read before the last barrier: the next tile resets it)
-#pragma unroll 1
-    for (int k = tid; k < total; k += k1_threads<TY>()) {
-        const int root = P[k] & 0xFFFF;
-        const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge index, or 0
-        const uint32_t rec = uint32_t(rs[root]) | (uint32_t(tag) << 16);
-        st_keep(Rt + k, rec);
-        // the first kRL runs of the first and last rows again in the edge
-        // brief: the boundary analysis' first round trip
-        if (k < kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeR0 + k, rec);
-        if (k >= rb_last && k < rb_last + kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeRL + (k - rb_last), rec);
-        // edge index -> root run (re, the run ends, is free after the flatten)
-        if (root == k && tag) re[tag - 1] = uint16_t(k);
-    }
-    __syncthreads();  // smem is reused by the next tile (rs / re / P are not rewritten
-                      // before its first barrier: the slot writes below still read them)
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
-    // the edge slots' initial entries (raster index << 32 | slot: every edge
-    // root its own set), four per thread = one whole 32-byte sector, so the
-    // boundary analysis' loads and atomics hit fully valid L2 sectors
-    {
-#pragma unroll 1
-        for (int j = tid; 4 * j < ne; j += k1_threads<TY>()) {
-            uint32_t v[8];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int i = 4 * j + q;
-                uint32_t gr = 0, sl = 0;
-                if (i < ne) {
-                    const int rr = rs[re[i]];
-                    gr = uint32_t((y0 + (rr >> 10)) * W + x0 + (rr & 1023));
-                    sl = edge_slot(g.ntiles, i, t);
-                }
-                v[2 * q] = sl;
-                v[2 * q + 1] = gr;
-            }
-            int4* sec = reinterpret_cast<int4*>(G + edge_slot(g.ntiles, 4 * j, t));
-            st_keep_v4(sec, make_int4(int(v[0]), int(v[1]), int(v[2]), int(v[3])));
-            st_keep_v4(sec + 1, make_int4(int(v[4]), int(v[5]), int(v[6]), int(v[7])));
-            if (g.strip) {  // strip marks: "no strip-boundary pixel seen yet" (ccl_strip.cuh)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (4 * j + q < ne) F[edge_slot(g.ntiles, 4 * j + q, t)] = -1;
-            }
-        }
-    }
-    if (g.epoch) {  // every output of the tile is written: publish it to the boundary analysis
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            st_release_u64(g.ready + t, g.epoch);
-        }
-    }
-}
-
-
-template <int TY, int CONN, bool VEC, int DBG = 0>
-__device__ __forceinline__ void k1_tile(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
-                                        ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
-                                        uint64_t* G, uint32_t* R, int32_t* E, int32_t* F, void* k1x, int warp,
-                                        int lane, bool v8) {
-    const TileId id = decode_tile<TY>(g, t);
-    const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
-    uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
-    const int tid = threadIdx.x;
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 0);
-
-#if CCL_K1_V8
-    // tall tiles (no room to hold the next tile in registers across the whole
-    // tile): this warp's rows are loaded here, all before any is converted
-    // (their L2 round trips overlap; the next tile was pulled into L2 by the
-    // bulk prefetch below while this one was processed)
-    if (VEC && !k1_prefetches<TY>()) k1_prefetch<TY>(img, g, t, warp, lane, v8, cur);
-#endif
-    // Alg. 1 l.3-8: the tile's pixels -> foreground masks (out-of-image pixels
-    // read as background, R5)
-#pragma unroll
-    for (int i = 0; i < (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); ++i) {
-        const int r = warp + i * k1_warps<TY>();
-        if (r >= TY) break;  // warp-uniform
-        const int y = id.y0 + r;
-        uint32_t m = 0;
-        if (VEC) {
-            uint4 v0 = cur.v[i][0], v1 = cur.v[i][1];
-#if CCL_K1_V8
-            // the lane's own 32 contiguous pixels: no cross-lane assembly
-            m = nz16(v0) | (nz16(v1) << 16);
-#else
-            if (!k1_prefetches<TY>()) {  // tall tiles: load in place (register budget)
-                v0 = v1 = make_uint4(0, 0, 0, 0);
-                if (y < g.H) {
-                    const uint8_t* row = im + size_t(y) * size_t(g.W) + id.x0;
-                    if (id.x0 + 16 * lane < g.W) v0 = ld_stream_u4(row + 16 * lane);
-                    if (id.x0 + 512 + 16 * lane < g.W) v1 = ld_stream_u4(row + 512 + 16 * lane);
-                }
-            }
-            // lane l holds pixels 16l.. and 512+16l..: assemble word l by shuffles
-            const uint32_t h0 = nz16(v0), h1 = nz16(v1);
-            const int src = (2 * lane) & 31;
-            const uint32_t a0 = __shfl_sync(kFull, h0, src), a1 = __shfl_sync(kFull, h0, src + 1);
-            const uint32_t b0 = __shfl_sync(kFull, h1, src), b1 = __shfl_sync(kFull, h1, src + 1);
-            m = lane < 16 ? (a0 | (a1 << 16)) : (b0 | (b1 << 16));
-#endif
-        } else {
-            const uint8_t* row = im + size_t(y < g.H ? y : 0) * size_t(g.W);
-#pragma unroll 4
-            for (int k = 0; k < kWords; ++k) {
-                const int x = id.x0 + (k << 5) + lane;
-                const bool fg = (y < g.H && x < g.W) ? (row[x] != 0) : false;
-                const uint32_t bal = __ballot_sync(kFull, fg);
-                if (lane == k) m = bal;
-            }
-        }
-        const int wg = id.tx * kWords + lane;
-        if (y < g.H && wg < g.WW) st_keep(bm + size_t(y) * g.WW + wg, m);
-        k1_row_init<TY>(sm, r, lane, m);
-    }
-    // the pixels are in the masks now: the same registers receive the block's
-    // next tile, in flight during the rest of this one
-    if (VEC && k1_prefetches<TY>() && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, v8, cur);
-    // tall tiles (no register room for a second tile): the next tile's rows
-    // are pulled into L2 with bulk prefetches instead, one per row
-    if (VEC && !k1_prefetches<TY>() && tnext < ntiles && warp == k1_warps<TY>() - 1 && lane < TY) {
-        const TileId nx = decode_tile<TY>(g, tnext);
-        const int y = nx.y0 + lane;
-        if (y < g.H) {
-            const uint8_t* row = img + size_t(nx.b) * size_t(g.npx) + size_t(y) * size_t(g.W) + nx.x0;
-            const unsigned bytes = unsigned(min(kTileW, g.W - nx.x0));
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"(bytes) : "memory");
-        }
-    }
-    if (tid < TY) sm.lc[tid] = -1;
-    else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
-    else if (tid == 2 * TY) sm.ecount = 0;
-    __syncthreads();
-    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
-
-    // run numbering: v (lane r) = first run id of row r+1
-    int v = lane < TY ? sm.rcnt[lane] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int u = __shfl_up_sync(kFull, v, d);
-        if (lane >= d) v += u;
-    }
-    const int total = __shfl_sync(kFull, v, TY - 1);  // block-uniform
-    if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
-    if (warp == 0 && lane == 0) sm.rbase[0] = 0;
-    if (total <= k1_cap<TY>()) {
-        k1_runs<TY, CONN, DBG>(sm, sm.rs, sm.re, sm.P, g, t, id, v, total, G, R, E, F, warp, lane);
-    } else {
-        char* slot = static_cast<char*>(k1x) + size_t(blockIdx.x) * k1x_slot_bytes<TY>();
-        constexpr int N = TY * kTileW / 2 + 8;
-        k1_runs<TY, CONN, DBG>(sm, reinterpret_cast<uint16_t*>(slot), reinterpret_cast<uint16_t*>(slot) + N,
-                               reinterpret_cast<int32_t*>(slot + 4 * N), g, t, id, v, total, G, R, E, F, warp, lane);
-    }
-}
-
-// ============================================================ K2: boundary
-// Boundary analysis (Alg. 2, §2.2): min-union of the local roots on the two
-// sides of every foreground edge that crosses a tile boundary (reading R9 /
-// R10).  The local roots come from K1's compact outputs -- the per-run records
-// of the tile rows next to a horizontal boundary and the column-root lists of
-// the tiles next to a vertical boundary -- so the only scattered accesses are
-// the union walks over the roots' parent entries in G.
-// K1's outputs are read with ld.global.cg (L2).
-
 // ---------------------------------------------- edge-slot union-find (K2)
 // G[s] = (X << 32) | parent slot, X = the parent's raster index (a root: its
 // own).  Same protocol as the 32-bit raster-indexed form it replaces (reading
@@ -1236,6 +584,657 @@ __device__ __forceinline__ int rec_root(uint32_t rec, int W, int x0, int y0) {
 __device__ __forceinline__ size_t tile_index(const Geom& g, int b, int ty, int tx) {
     return (size_t(b) * g.tiles_y + ty) * g.tiles_x + tx;
 }
+
+// =========================================================== K1: local merge
+// The tile's foreground is first turned into compact run lists (one entry per
+// row run, in raster order of the run starts) so every later step -- local UF,
+// flatten, edge output, per-run records -- runs one thread per run with all
+// lanes busy, instead of looping over the set bits of each lane's mask word.
+//
+// Coarse labeling (Alg. 1 l.9-24): the row scan + row-column unification in
+// the row direction is exact here -- every pixel's provisional label is its
+// run, the lowest equivalent label of its row segment (PAPER.md:230).
+// Local UF (Alg. 1 l.25-33): each run of row r >= 1 finds the runs of row r-1
+// it touches in O(1) from the masks (they are a contiguous index range of the
+// sorted upper run list) and min-unions with each (8-conn widens the contact
+// interval by one pixel on both sides: the NW / NE diagonals, reading R2/R10).
+// Persistent: each block walks tiles t = blockIdx.x, +gridDim.x, ...; the
+// 128-bit image loads of the NEXT tile are issued into registers before the
+// current tile is processed, so HBM reads overlap the shared-memory work.
+
+// One 32-px mask word of a K1 tile row.
+struct __align__(16) WordE {
+    uint32_t m;    // foreground mask
+    uint32_t s;    // run-start mask (tile-local runs)
+    uint32_t e;    // run-end mask
+    int32_t pad;   // number of run starts in the row before this word
+};
+
+// Run lists of a tile live in shared memory up to k1_cap runs (natural
+// images: a few hundred; i.i.d. noise at density 1/2: ~4096), which keeps the
+// block at 45 KB -- with one prefetch register set (44 registers) 5 blocks
+// (40 warps) per SM; measured: 4 blocks 46.8 us, 5 blocks 43.6 us on C3
+// texture (a cap of 4096 also allowed 5 blocks but sent half the noise tiles
+// to the scratch path).  A tile with more runs (period-2 stripes,
+// checkerboards: up to TY*512) keeps them in the block's slot of a global
+// scratch area instead (same code, L2-resident).
+#ifndef CCL_K1_CAP16
+#define CCL_K1_CAP16 4576
+#endif
+#ifndef CCL_K1_UF2
+#define CCL_K1_UF2 0  // two-step local UF (up-link forest, then the remaining pairs)
+#endif
+template <int TY>
+__host__ __device__ constexpr int k1_min_blocks() {
+    return TY > 16 ? (CCL_K1_T32 == 512 ? 2 : CCL_K1_BLOCKS32) : CCL_K1_BLOCKS;
+}
+
+template <int TY>
+struct K1Smem {
+    WordE wd[TY][kWords];
+    uint16_t rs[k1_cap<TY>() + 8];  // run k: start x | row << 10; rs[total] = sentinel row 63
+    uint16_t re[k1_cap<TY>() + 8];  // run k: end x
+    // parent over tile run ids (min-root forest).  After the flatten, a root
+    // whose component touches a tile edge carries bit 31 and (1 + its
+    // edge-list index) << 16; the low 16 bits are always the parent id.
+    int32_t P[k1_cap<TY>()];
+    int32_t ecount;                // edge-list length
+    int32_t lc[TY], rc[TY];        // roots of the left / right column pixels
+    int32_t rcnt[TY];              // runs per row
+    int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
+    int32_t ndefer;                // run-dense tiles of this block (listed in g.defer), labelled last
+};
+
+// find / merge of §2.1.3 (PAPER.md:311-313) over tile run ids.
+#ifdef CCL_STATS
+__device__ unsigned long long g_stat_k1_unions = 0, g_stat_k1_steps = 0, g_stat_k1_hops = 0;
+#endif
+__device__ __forceinline__ int find_r(int32_t* P, int a) {
+    volatile int32_t* V = P;
+    int p = V[a];
+    CCL_LOOP_GUARD(fr);
+    while (p != a) {
+        CCL_LOOP_TICK(fr);
+        CCL_STAT(g_stat_k1_hops);
+        const int gp = V[p];
+        if (gp != p) V[a] = gp;  // path halving: re-point at an ancestor
+        a = p;
+        p = gp;
+    }
+    return a;
+}
+
+// read-only find during the flatten: edge tags may be landing on roots, so
+// only the low 16 bits (the parent id) are followed
+__device__ __forceinline__ int find_r_ro(const int32_t* P, int a) {
+    const volatile int32_t* V = P;
+    int p = V[a] & 0xFFFF;
+    CCL_LOOP_GUARD(fro);
+    while (p != a) {
+        CCL_LOOP_TICK(fro);
+        a = p;
+        p = V[a] & 0xFFFF;
+    }
+    return a;
+}
+
+// Lock-free minimum-root union (reading R11): the larger root is re-pointed at
+// the smaller with atomicMin; if someone else re-linked it first, retry with
+// the value it was linked to.
+__device__ __forceinline__ void union_r(int32_t* P, int a, int b) {
+    CCL_STAT(g_stat_k1_unions);
+    while (true) {
+        CCL_STAT(g_stat_k1_steps);
+        a = find_r(P, a);
+        b = find_r(P, b);
+        if (a == b) return;
+        if (a < b) { int t = a; a = b; b = t; }
+        const int old = atomicMin(&P[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// K1's union call; profiling variants (DBG bit 8: skipped, bit 16: one
+// atomicMin without finds -- timing only, the labels are then wrong).
+template <int DBG>
+__device__ __forceinline__ void k1_union(int32_t* P, int a, int b) {
+    if (DBG & 8) return;
+    if (DBG & 16) {
+        atomicMin(&P[a], b);
+        return;
+    }
+    union_r(P, a, b);
+}
+
+// Profiling builds only (DBG bit 2): per-tile phase timestamps.
+__device__ unsigned long long* g_k1_stamps = nullptr;
+__device__ unsigned long long* g_k3_stamps = nullptr;
+__device__ unsigned long long* g_k2_stamps = nullptr;  // per K2 task: start, end (globaltimer ns)
+__device__ unsigned long long* g_k2_phase = nullptr;   // per horizontal K2 task: masks in, records in, 1st batch done
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void k1_stamp(unsigned t, int k) {
+    if (g_k1_stamps) g_k1_stamps[size_t(t) * 8 + k] = clock64();
+}
+__device__ __forceinline__ void k3_stamp(unsigned t, int k) {
+    if (g_k3_stamps) g_k3_stamps[size_t(t) * 8 + k] = clock64();
+}
+
+// rows per warp, and how many of them are prefetched into registers one tile
+// ahead: all of them for 8- and 16-row tiles; none for 32-row tiles, whose
+// four rows per warp are loaded at the start of their tile from L2 (the next
+// tile is pulled into L2 with bulk prefetches one tile ahead) -- measured on
+// C3 texture, 5 blocks/SM: 102.4 us/step vs 104.7 with two rows held in
+// registers and two loaded in place (CCL_K1_PF32=2), 105.4 with that at 4
+// blocks/SM (64 registers)
+template <int TY>
+__host__ __device__ constexpr int k1_rows_per_warp() { return (TY + k1_warps<TY>() - 1) / k1_warps<TY>(); }
+#ifndef CCL_K1_PF32
+#define CCL_K1_PF32 0
+#endif
+template <int TY>
+__host__ __device__ constexpr int k1_pf_rows() {
+    return k1_rows_per_warp<TY>() <= 2 ? k1_rows_per_warp<TY>() : CCL_K1_PF32;
+}
+
+template <int TY>
+struct ImgRegs {
+    uint4 v[k1_pf_rows<TY>() > 0 ? k1_pf_rows<TY>() : 1][2];  // row i of the warp: bytes 32*lane .. 32*lane + 31
+};
+
+
+// One lane's 32 contiguous pixels of a tile row: one 256-bit load when the
+// row is 32-byte aligned (W % 32 == 0 and an aligned image), else two 128-bit
+// loads (the row is 16-byte aligned on the vector path); pixels at or beyond
+// W read as background.  A warp instruction covers the whole 1024-px row.
+__device__ __forceinline__ void ld_px32(const uint8_t* p, int avail, bool v8, uint4& a, uint4& b) {
+    a = b = make_uint4(0, 0, 0, 0);
+    if (avail >= 32 && v8) {
+        asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
+    } else {
+        if (avail >= 16) a = ld_stream_u4(p);
+        if (avail >= 32) b = ld_stream_u4(p + 16);
+    }
+}
+
+template <int TY>
+__device__ __forceinline__ void k1_prefetch(const uint8_t* img, const Geom& g, unsigned t, int warp,
+                                            int lane, bool v8, ImgRegs<TY>& pf) {
+    const TileId id = decode_tile<TY>(g, t);
+    const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
+#pragma unroll
+    for (int i = 0; i < k1_pf_rows<TY>(); ++i) {
+        const int y = (warp + i * k1_warps<TY>() < TY) ? id.y0 + warp + i * k1_warps<TY>() : g.H;
+        pf.v[i][0] = pf.v[i][1] = make_uint4(0, 0, 0, 0);
+        const int x = id.x0 + 32 * lane;
+        if (y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, pf.v[i][0], pf.v[i][1]);
+    }
+}
+
+// Row r's mask word for this lane -> start / end masks, row-local run offsets.
+template <int TY>
+__device__ __forceinline__ void k1_row_init(K1Smem<TY>& sm, int r, int lane, uint32_t m) {
+    uint32_t pm = __shfl_up_sync(kFull, m, 1), nm = __shfl_down_sync(kFull, m, 1);
+    if (lane == 0) pm = 0;
+    if (lane == 31) nm = 0;
+    const uint32_t s = m & ~((m << 1) | (pm >> 31));
+    const uint32_t e = m & ~((m >> 1) | (nm << 31));
+    const int n = __popc(s);
+    int incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+    }
+    sm.wd[r][lane] = WordE{m, s, e, incl - n};
+    if (lane == 31) sm.rcnt[r] = incl;
+}
+
+// K1 from the run lists on: rs / re / P are the block's shared arrays or, for
+// a tile over k1_cap runs, its global scratch slot.
+// K1 on the rows [r0, r1) of a tile whose runs fit the shared-memory lists
+// (every tile is one such range unless it has more than k1_cap runs, e.g.
+// i.i.d. noise in 32-row tiles or period-2 stripes: then maximal row ranges
+// that fit, one after another).  Run ids are range-local (tile run id - base);
+// the records land at their tile run ids.  A range boundary inside the tile
+// is treated like a tile edge (its rows' roots become edge slots) and its
+// crossing edges are unioned in G by k1_internal_boundary.  ebase = the first
+// edge index of this range (a multiple of 4: whole 32-byte slot sectors).
+template <int TY, int CONN, int DBG, bool WHOLE>
+__device__ __forceinline__ int k1_range(K1Smem<TY>& sm, const Geom& g, unsigned t, const TileId& id, int v,
+                                         int r0_, int r1_, int ebase_, uint64_t* G, uint32_t* R, int32_t* E,
+                                         int32_t* F, int warp, int lane) {
+    constexpr int T1 = k1_threads<TY>(), NW1 = k1_warps<TY>();
+    // WHOLE: the tile is one range (every tile of a natural image): constant
+    // bounds, so the address arithmetic folds as before the ranges existed
+    const int r0 = WHOLE ? 0 : r0_, r1 = WHOLE ? TY : r1_, ebase = WHOLE ? 0 : ebase_;
+    uint16_t* __restrict__ rs = sm.rs;
+    uint16_t* __restrict__ re = sm.re;
+    int32_t* P = sm.P;
+    const int tid = threadIdx.x;
+    const int b0 = __shfl_sync(kFull, v, max(r0 - 1, 0));
+    const int base = r0 > 0 ? b0 : 0;                        // tile run id of the range's first run
+    const int total = __shfl_sync(kFull, v, r1 - 1) - base;  // runs of the range
+    // run lists: rs / re in raster order of the starts, P[k] = k
+#pragma unroll
+    for (int i = 0; i < (TY + NW1 - 1) / NW1; ++i) {
+        const int r = r0 + warp + i * NW1;
+        if (r >= r1) break;  // warp-uniform
+        const int rbr = __shfl_sync(kFull, v, max(r - 1, 0));
+        const int rb = (r > 0 ? rbr : 0) - base;
+        const WordE w = sm.wd[r][lane];
+        sm.wd[r][lane].pad = rb + w.pad;  // from here on: range run id of the word's first start
+        const int xb = lane << 5;
+        int ks = rb + w.pad;
+        int ke = ks - ((w.m & 1u) && !(w.s & 1u));  // a run open at the word start ends here
+        uint32_t sb = w.s, eb = w.e;
+        while (sb) {
+            const int bit = __ffs(sb) - 1;
+            sb &= sb - 1;
+            rs[ks] = uint16_t((xb + bit) | (r << 10));
+#if !CCL_K1_UF2
+            P[ks] = ks;
+#endif
+            ++ks;
+        }
+        while (eb) {
+            const int bit = __ffs(eb) - 1;
+            eb &= eb - 1;
+            re[ke++] = uint16_t(xb + bit);
+        }
+    }
+    if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
+    if (DBG & 1) {
+        __syncthreads();
+        return ebase;
+    }
+
+    // local UF.  The adjacencies between two rows form a monotone staircase of
+    // run pairs; every pair is (k, first upper neighbour of k) or (first lower
+    // neighbour of j, j) -- if j is the 2nd+ upper neighbour of k, j starts
+    // right of k's start, so it cannot reach k-1.  Each run therefore does at
+    // most two unions, found in O(1) from the masks: no fan-in serialisation.
+    constexpr int D = CONN == 8 ? 1 : 0;
+#if CCL_K1_UF2
+    // Column-direction coarse labeling first (Alg. 1 l.14-24 at run level,
+    // the A/B of profiles/r02_coarse_labeling_ab.txt): U1 links every run to
+    // its first upper neighbour with a plain store (a forest whose roots are
+    // their trees' minima), U2 unions only the remaining adjacencies.
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        int parent = k;
+        if (r > r0) {
+            const WordE uu = sm.wd[r - 1][p >> 5];
+            const uint32_t below = (1u << (p & 31)) - 1u;
+            const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
+            const int rsu = rs[ju];
+            if ((rsu >> 10) == r - 1 && (rsu & 1023) <= q) parent = ju;
+        }
+        P[k] = parent;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        if (r + 1 >= r1 || k == 0) continue;
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        const WordE ud = sm.wd[r + 1][p >> 5];
+        const uint32_t below = (1u << (p & 31)) - 1u;
+        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
+        const int rsd = rs[jd], rsp = rs[k - 1], ep = re[k - 1];
+        // jd touches k, and run k-1 (same row) touches jd too: k is a 2nd+ upper neighbour of jd
+        if ((rsd >> 10) == r + 1 && (rsd & 1023) <= q && (rsp >> 10) == r && ep + D >= (rsd & 1023))
+            k1_union<DBG>(P, jd, k);
+    }
+#else
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) {
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
+        // first runs of rows r-1 and r+1 touching [p, q] (both searches are
+        // issued before either union: the phase is bound by this chain)
+        const WordE uu = sm.wd[r > r0 ? r - 1 : r0][p >> 5];
+        const WordE ud = sm.wd[r + 1 < r1 ? r + 1 : r1 - 1][p >> 5];
+        const uint32_t below = (1u << (p & 31)) - 1u;
+        const int ju = uu.pad - ((uu.m & 1u) && !(uu.s & 1u)) + __popc(uu.e & below);
+        const int jd = ud.pad - ((ud.m & 1u) && !(ud.s & 1u)) + __popc(ud.e & below);
+        const int rsu = rs[ju], rsd = rs[jd];  // may be another row's run or the sentinel
+        if (r > r0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
+        if (r + 1 < r1 && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) k1_union<DBG>(P, jd, k);
+    }
+#endif
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
+    // flatten + Alg. 1 l.34-39 for tile-edge items only (reading R7 for the
+    // index conversion): every run points at its root; the first run to find
+    // that its root's component touches a tile edge (top / bottom row run,
+    // left / right column pixel, or a row next to a range boundary) claims the
+    // root (bit 31), takes the next edge index i of the tile and tags the root
+    // with 1 + i (claim order: any bijection works, the labels do not depend
+    // on it); the root becomes edge slot i * ntiles + t with entry (global
+    // raster index << 32) | slot.
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 4);
+    const int W = g.W, x0 = id.x0, y0 = id.y0;
+    const int last_row = min(TY, g.H - y0) - 1;  // (r1 - 1 >= last_row for the last range)
+    const int rl = min(r1 - 1, last_row);
+    // rows that border another tile (or, in strip mode, another strip) or range
+    const bool top = r0 > 0 || y0 > 0 || g.force_top;
+    const bool bottom = rl < last_row || y0 + TY < g.H || (g.force_bottom && y0 + TY >= g.H);
+    const bool left = x0 > 0, right = x0 + kTileW < W;
+    int32_t* Eh = E + size_t(t) * kEdgeCap;
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) {
+        const int root = find_r_ro(P, k);
+        if (root != k) P[k] = root;  // an ancestor: concurrent finds stay valid
+        const int rsk = rs[k];
+        const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
+        const bool hrow = (r == r0 && top) || (r == rl && bottom);
+        const bool lc = si == 0 && left, rc = ei == kTileW - 1 && right;
+        if (hrow || lc || rc) {
+            if (!(atomicOr(&P[root], int(0x80000000u)) & int(0x80000000u))) {
+                const int idx = ebase + atomicAdd(&sm.ecount, 1);
+                CCL_ASSERT(idx < edge_slots(TY));
+                P[root] = root | int(0x80000000u) | ((idx + 1) << 16);
+            }
+            if (lc) sm.lc[r] = k;  // the column pixel's run (its root's slot after the claims)
+            if (rc) sm.rc[r] = k;
+        }
+    }
+    if (DBG & 2) {
+        __syncthreads();
+        __syncthreads();
+        return ebase;
+    }
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 5);
+    // edge brief: header, column-root slots of the range's rows; per-run
+    // records for K3 / K2
+    const int ne = ebase + sm.ecount;  // (read before the last barrier: the next range / tile resets it)
+    const int rbl = __shfl_sync(kFull, v, max(last_row - 1, 0));
+    const int rb_last = last_row > 0 ? rbl : 0;  // tile run id of the last valid row's first run
+    if (tid == 0) {
+        st_keep(Eh, ne);
+        st_keep(Eh + 1, rb_last);
+    }
+    for (int j = tid; j < 2 * (r1 - r0); j += T1) {
+        const int r = r0 + (j >> 1);
+        const int k = (j & 1) ? sm.rc[r] : sm.lc[r];
+        int slot = -1;
+        if (k >= 0) slot = int(edge_slot(g.ntiles, ((P[P[k] & 0xFFFF] >> 16) & 0x7FFF) - 1, t));
+        st_keep(Eh + ((j & 1) ? kEdgeRC : kEdgeLC) + r, slot);
+    }
+    uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) {
+        const int root = P[k] & 0xFFFF;
+        const int tag = (P[root] >> 16) & 0x7FFF;  // 1 + edge index, or 0
+        const uint32_t rec = uint32_t(rs[root]) | (uint32_t(tag) << 16);
+        const int kt = base + k;  // tile run id
+        st_keep(Rt + kt, rec);
+        // the first kRL runs of the first and last rows again in the edge
+        // brief: the boundary analysis' first round trip
+        if (kt < kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeR0 + kt, rec);
+        if (kt >= rb_last && kt < rb_last + kRL) st_keep(reinterpret_cast<uint32_t*>(Eh) + kEdgeRL + (kt - rb_last), rec);
+        // edge index -> root run (re, the run ends, is free after the flatten)
+        if (root == k && tag) re[tag - 1 - ebase] = uint16_t(k);
+    }
+    __syncthreads();  // the slot writes below read rs / re: the next range / tile rewrites them only
+                      // after its own first barrier
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 6);
+    // the edge slots' initial entries (raster index << 32 | slot: every edge
+    // root its own set), four per thread = one whole 32-byte sector, so the
+    // boundary analysis' loads and atomics hit fully valid L2 sectors; a
+    // sector's unused tail (edge indices >= ne) holds harmless self-roots
+#pragma unroll 1
+    for (int j = tid; 4 * j < ne - ebase; j += T1) {
+        uint32_t vv[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = ebase + 4 * j + q;
+            uint32_t gr = 0x7FFFFFFEu;
+            if (i < ne) {
+                const int rr = rs[re[i - ebase]];
+                gr = uint32_t((y0 + (rr >> 10)) * W + x0 + (rr & 1023));
+            }
+            // strip marks (ccl_strip.cuh), the padding too: a run-dense tile's
+            // next range starts at the next sector, so padding slots lie below
+            // the tile's edge count and K3 resolves them (labels never used)
+            if (g.strip) F[edge_slot(g.ntiles, i, t)] = -1;
+            vv[2 * q] = edge_slot(g.ntiles, i, t);
+            vv[2 * q + 1] = gr;
+        }
+        int4* sec = reinterpret_cast<int4*>(G + edge_slot(g.ntiles, ebase + 4 * j, t));
+        st_keep_v4(sec, make_int4(int(vv[0]), int(vv[1]), int(vv[2]), int(vv[3])));
+        st_keep_v4(sec + 1, make_int4(int(vv[4]), int(vv[5]), int(vv[6]), int(vv[7])));
+    }
+    return ne;
+}
+
+// Unions of the foreground edges that cross the boundary above row rb of
+// tile t (a boundary between two row ranges of one tile): one warp, the
+// same pair extraction as the boundary analysis' horizontal tasks, from the
+// tile's masks (shared memory) and its just-written run records.
+template <int TY, int CONN>
+__device__ __forceinline__ void k1_internal_boundary(K1Smem<TY>& sm, const Geom& g, unsigned t, int v, int rb,
+                                                     uint64_t* G, const uint32_t* R, int lane) {
+    const uint32_t cur = sm.wd[rb][lane].m, up = sm.wd[rb - 1][lane].m;
+    uint32_t curL = __shfl_up_sync(kFull, cur, 1), upL = __shfl_up_sync(kFull, up, 1);
+    uint32_t curR = __shfl_down_sync(kFull, cur, 1), upR = __shfl_down_sync(kFull, up, 1);
+    if (lane == 0) { curL = 0; upL = 0; }
+    if (lane == 31) { curR = 0; upR = 0; }
+    const uint32_t sc = cur & ~((cur << 1) | (curL >> 31)), su = up & ~((up << 1) | (upL >> 31));
+    int ic = __popc(sc), iu = __popc(su);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(kFull, ic, d), c = __shfl_up_sync(kFull, iu, d);
+        if (lane >= d) { ic += a; iu += c; }
+    }
+    ic -= __popc(sc);
+    iu -= __popc(su);
+    const uint32_t o = cur & up, oL = curL & upL;
+    uint32_t ev = o & ~((o << 1) | (oL >> 31));
+    uint32_t ne = 0, nw = 0;
+    if (CONN == 8) {
+        const uint32_t cur_n = (cur >> 1) | (curR << 31), up_n = (up >> 1) | (upR << 31);
+        const uint32_t cur_p = (cur << 1) | (curL >> 31), up_p = (up << 1) | (upL >> 31);
+        ne = cur & ~cur_n & ~up & up_n;
+        nw = cur & ~cur_p & ~up & up_p;
+    }
+    const uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
+    const int base_c = __shfl_sync(kFull, v, rb - 1);  // tile run id of row rb's first run
+    const int bu = __shfl_sync(kFull, v, max(rb - 2, 0));
+    const int base_u = rb > 1 ? bu : 0;                  // ... of row rb - 1
+    unsigned long long last = ~0ull;
+    // the run containing pixel x of a row (word data of that row from a shuffle)
+    auto run_of = [&](uint32_t s, int pad, int x) {
+        const uint32_t sw = __shfl_sync(kFull, s, x >> 5);
+        const int pw = __shfl_sync(kFull, pad, x >> 5);
+        return pw + __popc(sw & (kFull >> (31 - (x & 31)))) - 1;
+    };
+    while (__any_sync(kFull, ev | ne | nw)) {
+        int x = 0, xu = 0;
+        const bool have = (ev | ne | nw) != 0;
+        if (ev) {
+            x = (lane << 5) + __ffs(ev) - 1;
+            ev &= ev - 1;
+            xu = x;
+        } else if (ne) {
+            x = (lane << 5) + __ffs(ne) - 1;
+            ne &= ne - 1;
+            xu = x + 1;
+        } else if (nw) {
+            x = (lane << 5) + __ffs(nw) - 1;
+            nw &= nw - 1;
+            xu = x - 1;
+        }
+        // every lane takes part in the shuffles (x = 0 for lanes without an event)
+        const int ia = run_of(sc, ic, x), ib = run_of(su, iu, xu);
+        int a = -1, b = -1;
+        if (have) {
+            a = rec_slot(__ldcg(Rt + base_c + ia), g.ntiles, t);
+            b = rec_slot(__ldcg(Rt + base_u + ib), g.ntiles, t);
+        }
+        warp_union_pairs(G, a, b, last);
+    }
+}
+
+
+// K1, first half of a tile: pixels -> masks, row runs, run numbering.
+// Returns v (lane r: tile run id of the first run of row r + 1).  INPLACE:
+// the tile's pixels are loaded here (run-dense tiles, processed after the
+// block's other tiles); else they were prefetched into cur, which then
+// receives the next tile.
+template <int TY, int CONN, bool VEC, bool INPLACE, int DBG = 0>
+__device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
+                                        ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
+                                        int warp, int lane, bool v8) {
+    const TileId id = decode_tile<TY>(g, t);
+    const uint8_t* im = img + size_t(id.b) * size_t(g.npx);
+    uint32_t* bm = bits + size_t(id.b) * size_t(g.nwords);
+    const int tid = threadIdx.x;
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 0);
+
+    // Alg. 1 l.3-8: the tile's pixels -> foreground masks (out-of-image pixels
+    // read as background, R5).  The rows not held in the prefetch registers
+    // (32-row tiles: the warp's last two; INPLACE: all) are loaded first.
+    constexpr int RPW = k1_rows_per_warp<TY>(), PFR = INPLACE ? 0 : k1_pf_rows<TY>();
+    constexpr int NL = RPW - PFR > 0 ? RPW - PFR : 1;
+    uint4 lv[NL][2];
+    if (VEC) {
+#pragma unroll
+        for (int i = PFR; i < RPW; ++i) {
+            const int r = warp + i * k1_warps<TY>(), y = id.y0 + r, x = id.x0 + 32 * lane;
+            lv[i - PFR][0] = lv[i - PFR][1] = make_uint4(0, 0, 0, 0);
+            if (r < TY && y < g.H) ld_px32(im + size_t(y) * size_t(g.W) + x, g.W - x, v8, lv[i - PFR][0], lv[i - PFR][1]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int r = warp + i * k1_warps<TY>();
+        if (r >= TY) break;  // warp-uniform
+        const int y = id.y0 + r;
+        uint32_t m = 0;
+        if (VEC) {
+            // the lane's own 32 contiguous pixels: no cross-lane assembly
+            const uint4 v0 = i < PFR ? cur.v[i < PFR ? i : 0][0] : lv[i >= PFR ? i - PFR : 0][0];
+            const uint4 v1 = i < PFR ? cur.v[i < PFR ? i : 0][1] : lv[i >= PFR ? i - PFR : 0][1];
+            m = nz16(v0) | (nz16(v1) << 16);
+        } else {
+            const uint8_t* row = im + size_t(y < g.H ? y : 0) * size_t(g.W);
+#pragma unroll 4
+            for (int k = 0; k < kWords; ++k) {
+                const int x = id.x0 + (k << 5) + lane;
+                const bool fg = (y < g.H && x < g.W) ? (row[x] != 0) : false;
+                const uint32_t bal = __ballot_sync(kFull, fg);
+                if (lane == k) m = bal;
+            }
+        }
+        const int wg = id.tx * kWords + lane;
+        if (y < g.H && wg < g.WW) st_keep(bm + size_t(y) * g.WW + wg, m);
+        k1_row_init<TY>(sm, r, lane, m);
+    }
+    // the pixels are in the masks now: the prefetch registers receive the
+    // block's next tile, in flight during the rest of this one ...
+    if (!INPLACE && VEC && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, v8, cur);
+    // ... and its other rows are pulled into L2 with bulk prefetches
+    if (!INPLACE && VEC && RPW > k1_pf_rows<TY>() && tnext < ntiles && warp == k1_warps<TY>() - 1 &&
+        lane < TY - k1_pf_rows<TY>() * k1_warps<TY>()) {
+        const TileId nx = decode_tile<TY>(g, tnext);
+        const int y = nx.y0 + k1_pf_rows<TY>() * k1_warps<TY>() + lane;
+        if (y < g.H) {
+            const uint8_t* row = img + size_t(nx.b) * size_t(g.npx) + size_t(y) * size_t(g.W) + nx.x0;
+            const unsigned bytes = unsigned(min(kTileW, g.W - nx.x0));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"(bytes) : "memory");
+        }
+    }
+    if (tid < TY) sm.lc[tid] = -1;
+    else if (tid < 2 * TY) sm.rc[tid - TY] = -1;
+    else if (tid == 2 * TY) sm.ecount = 0;
+    __syncthreads();
+    if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 1);
+
+    // run numbering: v (lane r) = first run id of row r+1
+    int v = lane < TY ? sm.rcnt[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += u;
+    }
+    if (warp == 0 && lane < TY) sm.rbase[lane + 1] = v;
+    if (warp == 0 && lane == 0) sm.rbase[0] = 0;
+    return v;
+}
+
+// K1 publishes a finished tile to the boundary analysis (K1 -> K2 overlap)
+__device__ __forceinline__ void k1_publish(const Geom& g, unsigned t) {
+    if (g.epoch) {  // every output of the tile is written
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_u64(g.ready + t, g.epoch);
+        }
+    }
+}
+
+// K1, second half of a run-dense tile (more runs than the shared-memory
+// lists hold): maximal row ranges that fit, each labelled alone, then the
+// range boundaries unioned in G like tile boundaries.
+template <int TY, int CONN, int DBG = 0>
+__device__ __forceinline__ void k1_dense(K1Smem<TY>& sm, const Geom& g, unsigned t, int v, uint64_t* G, uint32_t* R,
+                                         int32_t* E, int32_t* F, int warp, int lane) {
+    const int tid = threadIdx.x;
+    const TileId id = decode_tile<TY>(g, t);
+    // maximal row ranges whose runs fit the shared-memory lists (one range
+    // unless the tile is run-dense); each is labelled alone, then the range
+    // boundaries are unioned in G like tile boundaries
+    int r0 = 0, ebase = 0;
+    uint32_t inner = 0;  // rows that start a range after the first
+    while (r0 < TY) {  // block-uniform
+        const int b0 = __shfl_sync(kFull, v, max(r0 - 1, 0));
+        const int base = r0 > 0 ? b0 : 0;
+        const unsigned fit = __ballot_sync(kFull, lane >= r0 && lane < TY && v - base <= k1_cap<TY>());
+        const int r1 = 32 - __clz(fit);  // >= r0 + 1: one row has <= 512 runs
+        if (r0 > 0) {
+            inner |= 1u << r0;
+            __syncthreads();  // the previous range's slot writes have read rs / re / ecount
+            if (tid == 0) sm.ecount = 0;
+        }
+        const int ne = k1_range<TY, CONN, DBG, false>(sm, g, t, id, v, r0, r1, ebase, G, R, E, F, warp, lane);
+        ebase = (ne + 3) & ~3;  // the next range starts on a whole slot sector
+        r0 = r1;
+    }
+    if (inner) {
+        __syncthreads();  // every range's records and slot entries are written
+        int i = 0;
+        for (uint32_t m = inner; m; m &= m - 1, ++i)
+            if (warp == i % k1_warps<TY>()) k1_internal_boundary<TY, CONN>(sm, g, t, v, __ffs(m) - 1, G, R, lane);
+        __syncthreads();  // (the next tile rewrites the row words these read)
+    }
+    k1_publish(g, t);
+}
+
+// ============================================================ K2: boundary
+// Boundary analysis (Alg. 2, §2.2): min-union of the local roots on the two
+// sides of every foreground edge that crosses a tile boundary (reading R9 /
+// R10).  The local roots come from K1's compact outputs -- the per-run records
+// of the tile rows next to a horizontal boundary and the column-root lists of
+// the tiles next to a vertical boundary -- so the only scattered accesses are
+// the union walks over the roots' parent entries in G.
+// K1's outputs are read with ld.global.cg (L2).
+
 
 // The horizontal boundary above tile (b, band >= 1, tx); one warp.
 #ifndef CCL_PAIRS_PER_LANE
@@ -1501,7 +1500,7 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
                                                              uint32_t* __restrict__ R,
                                                              int32_t* __restrict__ E,
                                                              int32_t* __restrict__ F,
-                                                             void* __restrict__ k1x, unsigned ntiles) {
+                                                             unsigned ntiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem<TY>& sm = *reinterpret_cast<K1Smem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1511,16 +1510,35 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     // on the per-tile ready flags)
     if (g.epoch) pdl_launch_dependents();
     if (t >= ntiles) return;
-    constexpr bool PF = VEC && k1_prefetches<TY>();
+    constexpr bool PF = VEC;  // the first tile's register rows (k1_pf_rows)
     // one register set: loaded with tile t before the loop, then refilled with
     // the block's next tile as soon as the current one is in the masks
     // 256-bit image loads need 32-byte aligned rows
     const bool v8 = ((g.W & 31) == 0) && ((reinterpret_cast<uintptr_t>(img) & 31) == 0);
     ImgRegs<TY> a;
     if (PF) k1_prefetch<TY>(img, g, t, warp, lane, v8, a);
+    if (threadIdx.x == 0) sm.ndefer = 0;
+    // every tile whose runs fit the shared-memory lists is labelled as one
+    // range; run-dense tiles are deferred to the loop below, so the range
+    // machinery stays out of this loop's code and registers
     while (t < ntiles) {
-        k1_tile<TY, CONN, VEC, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, G, R, E, F, k1x, warp, lane, v8);
+        const int v = k1_masks<TY, CONN, VEC, false, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, warp, lane, v8);
+        if (__shfl_sync(kFull, v, TY - 1) <= k1_cap<TY>()) {  // block-uniform
+            k1_range<TY, CONN, DBG, true>(sm, g, t, decode_tile<TY>(g, t), v, 0, TY, 0, G, R, E, F, warp, lane);
+            k1_publish(g, t);
+        } else if (threadIdx.x == 0) {
+            // (block b's list: g.defer[b * per ..], per = ceil(ntiles / grid) slots)
+            g.defer[size_t(blockIdx.x) * ((ntiles + gridDim.x - 1) / gridDim.x) + sm.ndefer++] = t;
+        }
         t += gridDim.x;
+    }
+    __syncthreads();
+    const int nd = sm.ndefer;
+    for (int i = 0; i < nd; ++i) {
+        const unsigned td = unsigned(__ldcg(g.defer + size_t(blockIdx.x) * ((ntiles + gridDim.x - 1) / gridDim.x) + i));
+        const int v = k1_masks<TY, CONN, VEC, true, DBG>(sm, img, g, td, a, ntiles, ntiles, bits, warp, lane, v8);
+        k1_dense<TY, CONN, DBG>(sm, g, td, v, G, R, E, F, warp, lane);
+        __syncthreads();  // smem is reused by the next deferred tile
     }
 }
 
@@ -1568,6 +1586,39 @@ __global__ void __launch_bounds__(256) k_resolve(Geom g, uint64_t* __restrict__ 
     }
 }
 
+// Strip mode (ccl_strip.cuh): the final label of an edge root on a strip
+// boundary row is the minimum label of its slot set in the slot union-find.
+struct StripFinal {
+    const int32_t* F;         // F[root slot] = INT_MAX - its first boundary slot, or -1
+    uint64_t* P;              // slot union-find over the k * 2W boundary slots
+    const int32_t* gathered;  // all ranks' send buffers (labels, reps)
+    int W, slot0;             // slot0 = this rank's first slot (rank * 2W)
+};
+__device__ __forceinline__ uint64_t slot_find(uint64_t* P, const int32_t* gathered, int W, unsigned s);
+
+// Final label of edge root i of tile t: its root in G (pointer jumping), and
+// in strip mode (!RES) for a root on a strip boundary the slot set's minimum.
+template <bool RES>
+__device__ __forceinline__ int edge_label(const Geom& g, uint64_t* G, const StripFinal& sf, unsigned t, int i) {
+    const uint64_t w = resolve_slot(G, edge_slot(g.ntiles, i, t));
+    int lab = int(w >> 32) + 1 + g.label_off;
+    if (!RES) {
+        const int v = __ldcg(sf.F + unsigned(w));
+#ifdef CCL_CHECK
+        if (v < -1 || (v >= 0 && INT_MAX - v >= 2 * sf.W))
+            printf("edge_label: tile %u edge %d root entry %llx F %d\n", t, i, (unsigned long long)w, v);
+#endif
+        CCL_ASSERT(v == -1 || (v >= 0 && INT_MAX - v < 2 * sf.W));
+        if (v >= 0) lab = int(slot_find(sf.P, sf.gathered, sf.W, unsigned(sf.slot0 + (INT_MAX - v))) >> 32);
+    }
+    return lab;
+}
+
+// The helper warp's shared slot holds the first kFlCap edge labels of a tile
+// (texture tiles use a few tens; only tiles labelled in several row ranges
+// exceed it -- the label table resolves those few entries itself).
+constexpr int kFlCap = 1088;
+
 // ================================================================ K3: link
 // Final link (§2.3).  Per tile:
 //  1. row runs re-derived from the bit mask (run numbering only, no
@@ -1603,7 +1654,7 @@ struct __align__(1024) LinkSmem {
     LWord wd[TY][kWords];
     int32_t lab[kLabCap];            // final label of tile run k (current row window)
     uint4 rc[kRunCache / 4];         // first run records of the tile (prefetched)
-    int32_t fl[2][edge_slots(TY)];   // final labels of the edge roots of tiles j, j+1 (helper warp)
+    int32_t fl[2][kFlCap];           // final labels of the edge roots i < kFlCap of tiles j, j+1 (helper warp)
     int32_t produced;                // tiles whose fl slot the helper warp has filled
     int32_t consumed;                // tiles whose fl slot the compute warps are done with
     int32_t rcnt[TY];
@@ -1669,10 +1720,11 @@ __device__ __forceinline__ int selp_nz(uint32_t x, int a, int b) {
 // group q = 8*w + g (word w, group g within the word) lives at 8*w + (g ^ (w & 7)).
 __device__ __forceinline__ int swz(int w, int g) { return (w << 3) + (g ^ (w & 7)); }
 
-template <int TY, int CONN, bool VEC, bool TMA, int DBG = 0>
+template <int TY, int CONN, bool VEC, bool TMA, bool RES, int DBG = 0>
 __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const uint32_t* bits, unsigned t, int j,
                                         const LinkRegs<TY>& cur, const uint32_t* R, int32_t* out,
-                                        const CUtensorMap* tmap, int warp, int lane) {
+                                        const CUtensorMap* tmap, int warp, int lane, uint64_t* G,
+                                        const StripFinal& sf) {
     const TileId id = decode_tile<TY>(g, t);
     int32_t* ob = out + size_t(id.b) * size_t(g.npx);
     const uint32_t* Rt = R + size_t(t) * runs_per_tile_cap<TY>();
@@ -1730,7 +1782,7 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
             const int e = int(rec >> 16);  // 1 + edge-list index, or 0
             const int rr = int(rec & 0x7FFFu);
             int lab = (y0 + (rr >> 10)) * W + x0 + (rr & 1023) + 1 + g.label_off;
-            if (e) lab = Fl[e - 1];
+            if (e) lab = e <= kFlCap ? Fl[e - 1] : edge_label<RES>(g, G, sf, t, e - 1);
             sm.lab[k - base] = lab;
         }
         k3_sync();
@@ -1842,29 +1894,12 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
 // in F.  k3_resolve_tile does one tile's roots i = first, first + stride, ...
 constexpr int kK3Threads = kThreads + 32;  // 8 compute warps + the helper warp
 
-// Strip mode (ccl_strip.cuh): the final label of an edge root on a strip
-// boundary row is the minimum label of its slot set in the slot union-find.
-struct StripFinal {
-    const int32_t* F;         // F[root slot] = INT_MAX - its first boundary slot, or -1
-    uint64_t* P;              // slot union-find over the k * 2W boundary slots
-    const int32_t* gathered;  // all ranks' send buffers (labels, reps)
-    int W, slot0;             // slot0 = this rank's first slot (rank * 2W)
-};
-__device__ __forceinline__ uint64_t slot_find(uint64_t* P, const int32_t* gathered, int W, unsigned s);
 
 template <bool RES>
 __device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, uint64_t* G,
                                                 const StripFinal& sf, unsigned t, int first, int stride) {
-    const int n = __ldcg(E + size_t(t) * kEdgeCap);
-    for (int i = first; i < n; i += stride) {
-        const uint64_t w = resolve_slot(G, edge_slot(g.ntiles, i, t));
-        int lab = int(w >> 32) + 1 + g.label_off;
-        if (!RES) {  // strip mode
-            const int v = __ldcg(sf.F + unsigned(w));
-            if (v >= 0) lab = int(slot_find(sf.P, sf.gathered, sf.W, unsigned(sf.slot0 + (INT_MAX - v))) >> 32);
-        }
-        slot[i] = lab;
-    }
+    const int n = min(__ldcg(E + size_t(t) * kEdgeCap), kFlCap);
+    for (int i = first; i < n; i += stride) slot[i] = edge_label<RES>(g, G, sf, t, i);
 }
 
 #ifndef CCL_K3_COOP
@@ -1942,11 +1977,11 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
     int j = 0;
     while (true) {
         if (j > 0 && t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, j++, a, R, out, &tmap, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, RES, DBG>(sm, g, bits, t, j++, a, R, out, &tmap, warp, lane, G, F);
         t += gridDim.x;
         if (t >= ntiles) break;
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, a);
-        k3_tile<TY, CONN, VEC, TMA, DBG>(sm, g, bits, t, j++, b, R, out, &tmap, warp, lane);
+        k3_tile<TY, CONN, VEC, TMA, RES, DBG>(sm, g, bits, t, j++, b, R, out, &tmap, warp, lane, G, F);
         t += gridDim.x;
         if (t >= ntiles) break;
     }

@@ -11,7 +11,8 @@
 //   S2 exclusive scan of the chunk counts per image (component ids);
 //   S3 each root gets its id (rank) in the sparse map M[root] and initialises
 //      its output record;
-//   S4 every foreground pixel is counted in record M[label - 1]: a warp walks
+//   S4 every foreground pixel is counted in record M[label - 1] (and, when
+//      asked, written to the relabelled map as M[label - 1] + 1): a warp walks
 //      its own contiguous range of 32-px segments; within a segment, runs of
 //      equal (component, row) have closed-form statistics (area = length,
 //      x range, coordinate sums); the run that reaches a segment's end is
@@ -178,7 +179,7 @@ __device__ __forceinline__ void add_global(ccl_component_t* e, int area, int x0,
 // of image blockIdx.y; each block aggregates in its shared table)
 __global__ void __launch_bounds__(kT) k_stats_accum(const int32_t* __restrict__ labels, long long npx, int W,
                                                     const int32_t* __restrict__ M, ccl_component_t* __restrict__ out,
-                                                    long long max_components) {
+                                                    long long max_components, int32_t* __restrict__ relabel) {
     __shared__ Acc a;
     const int b = blockIdx.y;
     const int32_t* L = labels + size_t(b) * size_t(npx);
@@ -246,6 +247,14 @@ __global__ void __launch_bounds__(kT) k_stats_accum(const int32_t* __restrict__ 
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) cv[u] = lv[u] > 0 ? __ldg(Mb + lv[u] - 1) : -1;
+        if (relabel) {  // the compact numbering 1..K: component id + 1, background 0
+            int32_t* Rb = relabel + size_t(b) * size_t(npx);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long i = (sb + u) * 32 + lane;
+                if (sb + u < s1 && i < npx) __stcs(Rb + i, cv[u] + 1);
+            }
+        }
         // one loop body for the U segments (a fully unrolled body thrashed the
         // instruction cache: 30 % of the stall samples); cv[] rotates so that
         // every index stays static

@@ -184,3 +184,15 @@ def test_strip_bounds_partition(ccl):
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+
+
+def test_default_tile_rows(ccl):
+    """The tile_rows = 0 rule: one of 8 / 16 / 32, never shorter for more work."""
+    prev = 0
+    for H in (16, 512, 2048, 8192, 32768):
+        ty = ccl.default_tile_rows(1, H, 8192)
+        assert ty in (8, 16, 32)
+        assert ty >= prev
+        prev = ty
+    with pytest.raises(ValueError):
+        ccl.default_tile_rows(1, 0, 5)

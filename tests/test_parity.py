@@ -331,3 +331,21 @@ def test_strips_c5_shape_sampled(ccl):
     t = torch.from_numpy(img).cuda()
     got = ccl.label_strips_emulated(t, 8, 8).cpu().numpy()
     assert_same(got, oracle.label_bfs(img, 8), "C5-like strips")
+
+
+@pytest.mark.parametrize("conn", CONNS)
+def test_strips_default_tile32(ccl, conn):
+    """Strips tall enough that the library's default tile height is 32 rows
+    (the C5 geometry's choice) -- dense noise tiles included, whose row ranges
+    meet the strip marks."""
+    import torch
+    H, W = 5000, 8192
+    assert ccl.default_tile_rows(1, H // 2, W) == 32
+    for name, img in [("texture", synth.texture(H, W, seed=41, density=0.5)),
+                      ("noise", synth.noise(H, W, 0.5, seed=42)),
+                      ("perc", synth.noise(H, W, synth.percolation_density(conn), seed=43))]:
+        want = oracle.label_bfs(img, conn)
+        t = torch.from_numpy(img).cuda()
+        for k in (1, 2):
+            got = ccl.label_strips_emulated(t, k, conn).cpu().numpy()
+            assert_same(got, want, f"strips {name} k={k} (32-row tiles)")

@@ -142,3 +142,57 @@ def test_stats_abi_errors(ccl):
     assert lib.ccl_component_stats_async(None, 1, 64, 64, 0, None, None, None, 0, None) == 2   # max_components < 1
     assert lib.ccl_component_stats_async(None, 1, 64, 64, 10, None, None, None, 0, None) == 1  # NULL
     assert lib.ccl_component_stats_async(None, 0, 64, 64, 10, None, None, None, 0, None) == 0  # B = 0
+
+
+# ------------------------------------------------- compact 1..K relabel
+def loop_relabel(L):
+    """The renumbering written out: labels visited in increasing order get 1, 2, ..."""
+    ids = {}
+    for l in sorted({int(v) for v in np.asarray(L).ravel() if v != 0}):
+        ids[l] = len(ids) + 1
+    out = np.zeros(L.shape, np.int32)
+    for idx, v in np.ndenumerate(L):
+        if v:
+            out[idx] = ids[int(v)]
+    return out
+
+
+@pytest.mark.parametrize("conn", (4, 8))
+def test_oracle_relabel_vs_loop_and_invariants(conn):
+    rng = np.random.default_rng(11)
+    for k in range(60):
+        H, W = int(rng.integers(1, 14)), int(rng.integers(1, 14))
+        img = (rng.random((H, W)) < rng.uniform(0.2, 0.8)).astype(np.uint8)
+        L = oracle.label_bfs(img, conn)
+        R = oracle.relabel_compact(L)
+        assert np.array_equal(R, loop_relabel(L)), f"random {k}"
+        # invariants: background stays 0; equal labels <-> equal ids; order
+        # preserved; the ids are exactly 1..K
+        assert np.array_equal(R == 0, L == 0)
+        fg = L != 0
+        pairs = set(zip(L[fg].tolist(), R[fg].tolist()))
+        assert len(pairs) == len({p[0] for p in pairs}) == len({p[1] for p in pairs})
+        srt = sorted(pairs)
+        assert [p[1] for p in srt] == list(range(1, len(srt) + 1))
+    # closed form: a checkerboard under 4-connectivity (every pixel its own
+    # component) renumbers to 1, 2, 3, ... along the raster order of the fg pixels
+    img = synth.checkerboard(6, 7) != 0
+    R = oracle.relabel_compact(oracle.label_bfs(img.astype(np.uint8), 4))
+    assert R[img].tolist() == list(range(1, int(img.sum()) + 1))
+
+
+@pytest.mark.gpu
+def test_gpu_relabel_matches_oracle():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1708_08180_b200 as ccl
+    cases = [synth.texture(1024, 2048, seed=21, density=0.5), synth.noise(600, 1100, 0.55, seed=22),
+             synth.blobs(777, 1031, seed=23, rmin=4, rmax=40), synth.texture(8192, 8192, seed=3001, density=0.5)]
+    for img in cases:
+        for conn in (4, 8):
+            lab = ccl.label(torch.from_numpy(img).cuda(), conn)
+            counts, st, rl = ccl.component_stats(lab, relabel=True)
+            want = oracle.relabel_compact(lab.cpu().numpy())
+            assert np.array_equal(rl.cpu().numpy(), want), f"{img.shape} conn={conn}"
+            assert int(counts[0]) == int(want.max())

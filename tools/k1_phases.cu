@@ -12,7 +12,6 @@
 #define CCL_K2_PHASES 1
 #include "../paper_1708_08180_b200/csrc/ccl_kernels.cuh"
 #include <cudaTypedefs.h>
-static void* g_k1x = nullptr;  // K1 overflow scratch
 
 #define CK(x)                                                                          \
     do {                                                                               \
@@ -82,7 +81,7 @@ void run_k1(const char* name, const uint8_t* img, ccl::Geom g, uint32_t* bits, u
     auto k = ccl::k_local_merge<TY, CONN, true, DBG>;
     size_t smem = sizeof(ccl::K1Smem<TY>);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    float us = timeit([&] { k<<<grid, ccl::k1_threads<TY>(), smem>>>(img, g, bits, G, R, E, g_F, g_k1x, ntiles); }, flush, fb);
+    float us = timeit([&] { k<<<grid, ccl::k1_threads<TY>(), smem>>>(img, g, bits, G, R, E, g_F, ntiles); }, flush, fb);
     printf("%-34s grid %6d  %8.1f us\n", name, grid, us);
 }
 
@@ -109,15 +108,14 @@ int main(int argc, char** argv) {
     void* flush;
     const size_t fb = size_t(512) << 20;
     CK(cudaMalloc(&img, n));
-    CK(cudaMalloc(&G, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 8));
+    CK(cudaMalloc(&G, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 8 * 4));
     CK(cudaMalloc(&out, n * 4));
     CK(cudaMalloc(&bits, n / 8 + 4096));
     CK(cudaMalloc(&R, 2 * n + 65536));
     CK(cudaMalloc(&E, (n / 1024 / 8 + 64) * ccl::kEdgeCap * 4));
-    CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 4));
+    CK(cudaMalloc(&F, (n / 1024 / 8 + 64) * ccl::edge_slots(8) * 4 * 4));
     g_F = F;
     CK(cudaMalloc(&flush, fb));
-    CK(cudaMalloc(&g_k1x, size_t(1024) * ccl::k1x_slot_bytes<32>()));
     unsigned* sink;
     CK(cudaMalloc(&sink, 64));
     CK(cudaMemcpy(img, h.data(), n, cudaMemcpyHostToDevice));
@@ -151,6 +149,10 @@ int main(int argc, char** argv) {
     g.label_off = g.force_top = g.force_bottom = 0;
     g.k3_early = 1;
     g.ntiles = ntiles;
+    g.epoch = 0;
+    g.ready = nullptr;
+    g.strip = 0;
+    CK(cudaMalloc(&g.defer, size_t(ntiles) * 4 + 4096));
     for (int per_sm : {4, 5}) {
         int grid = std::min<int>(ntiles, sms * per_sm);
         char nm[64];
@@ -198,7 +200,7 @@ int main(int argc, char** argv) {
         float tot2 = 0;
         for (int i = 0; i < 23; ++i) {
             CK(cudaMemsetAsync(flush, i, fb));
-            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
             CK(cudaEventRecord(a));
             k2<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
             CK(cudaEventRecord(b));
@@ -225,7 +227,7 @@ int main(int argc, char** argv) {
         float tot2 = 0;
         for (int i = 0; i < 23; ++i) {
             CK(cudaMemsetAsync(flush, i, fb));
-            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
             touch_k1_outputs<<<sms * 4, 256>>>(bits, g.nwords, R, ccl::runs_per_tile_cap<TY>(), E, G, ntiles, sink);
             CK(cudaEventRecord(a));
             ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
@@ -249,7 +251,7 @@ int main(int argc, char** argv) {
         for (int ver = 0; ver < 1; ++ver) {
         CK(cudaMemset(ph, 0, size_t(nt) * 32));
         if (ver == 0) CK(cudaMemcpyToSymbol(ccl::g_k2_phase, &ph, sizeof(ph)));
-        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
         auto kt = ccl::k_boundary<TY, 8, 8>;
         kt<<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v, 0);
         CK(cudaDeviceSynchronize());
@@ -298,7 +300,7 @@ int main(int argc, char** argv) {
             CK(cudaMalloc(&ts, size_t(nt) * 16));
             CK(cudaMemset(ts, 0, size_t(nt) * 16));
             CK(cudaMemcpyToSymbol(ccl::g_k2_taskstat, &ts, sizeof(ts)));
-            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
             ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
             CK(cudaDeviceSynchronize());
             std::vector<unsigned> hts(size_t(nt) * 4);
@@ -324,7 +326,7 @@ int main(int argc, char** argv) {
         CK(cudaMemcpyToSymbol(ccl::g_k2_stamps, &np, sizeof(np)));
     }
     {
-        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
         ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
         float us = timeit([&] { ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles); }, flush, fb);
         printf("%-34s %8.1f us\n", "K2b resolve", us);
@@ -335,7 +337,7 @@ int main(int argc, char** argv) {
         unsigned long long z = 0, u, st, nf, nh, mh;
         CK(cudaMemcpyToSymbol(ccl::g_stat_unions, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_steps, &z, 8));
-        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+        k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpyToSymbol(ccl::g_stat_finds, &z, 8));
         CK(cudaMemcpyToSymbol(ccl::g_stat_hops, &z, 8));
@@ -353,7 +355,7 @@ int main(int argc, char** argv) {
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_unions, &z, 8));
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_steps, &z, 8));
             CK(cudaMemcpyToSymbol(ccl::g_stat_k1_hops, &z, 8));
-            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+            k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
             CK(cudaDeviceSynchronize());
             CK(cudaMemcpyFromSymbol(&ku, ccl::g_stat_k1_unions, 8));
             CK(cudaMemcpyFromSymbol(&ks, ccl::g_stat_k1_steps, 8));
@@ -365,7 +367,7 @@ int main(int argc, char** argv) {
     }
 #endif
     // K3 (after K1 + K2), with stamps
-    k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, g_k1x, ntiles);
+    k1<<<grid1, ccl::k1_threads<TY>(), sm1>>>(img, g, bits, G, R, E, F, ntiles);
     ccl::k_boundary<TY, 8, 0><<<unsigned(bh + bv), 256>>>(g, bits, R, E, G, n_h, n_v);
     ccl::k_resolve<TY><<<std::min<unsigned>((ntiles + 7) / 8, 148 * 16), 256>>>(g, G, E, F, ntiles);
     auto k3 = ccl::k_link<TY, 8, true, true, true, 0>;
