@@ -435,10 +435,10 @@ def run_ours(args, rank, world, local):
         bpp = {"k1_local_merge": K1_BYTES_PER_PX, "k3_link": K3_BYTES_PER_PX}.get(dom)
         if bpp is not None:
             ach = bpp * px_rank / (kern[dom] / 1e3) / 1e9
-            traffic = load_traffic(name, dom)
+            traffic = load_traffic(name + (" 4-conn" if conn == 4 else ""), dom)
             line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                                 "unit": "GB/s", "frac": round(ach / peak, 4),
-                                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/)",
+                                "traffic": traffic, "traffic_unit": "bytes per launch: max(DRAM read + write, DRAM read + L2 write-in), ncu, profiles/ncu_traffic.json",
                                 "algorithmic_bytes_per_launch": int(bpp * px_rank),
                                 "bytes_per_px": bpp, "peak_source": peak_src,
                                 "share_of_step": round(kern[dom] / sum(kern.values()), 3)}

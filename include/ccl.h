@@ -65,13 +65,15 @@ const char* ccl_status_string(ccl_status_t status);
 int ccl_last_cuda_error(void);
 
 /* Device workspace (bytes) needed by the *_async entry points for B images of
- * H x W (about 3.7 bytes per pixel): the bit-packed
- * foreground mask (one bit per pixel, rows padded to 32 px), per-run records
- * (sized for the worst case, alternating pixels), per-tile edge briefs, the
- * boundary analysis' union-find over edge slots (8 bytes per slot, one slot
- * per edge-touching local root, at most 1040-1088 per tile), the strip marks,
- * and the K1 scratch slots for run-dense tiles.  Sized for every tile
- * configuration.  Returns 0 for invalid arguments. */
+ * H x W (3.7 bytes per pixel for 8192 x 8192): the
+ * bit-packed foreground mask (1/8 B/px, rows padded to 32 px), per-run records
+ * (4 B per run, sized for the worst case of alternating pixels: 2 B/px),
+ * per-tile edge briefs (136 ints per 8-row tile), the boundary analysis'
+ * union-find over edge slots (8 bytes per slot, one slot per edge-touching
+ * local root; per tile enough for the worst case of the tile configuration
+ * that needs the most -- 1.5 B/px), the K1 -> K2 ready flags and the lists of
+ * run-dense tiles.  Sized for every tile configuration.  The strip stages
+ * need more (ccl_strip_workspace_bytes).  Returns 0 for invalid arguments. */
 size_t ccl_workspace_bytes(int64_t B, int64_t H, int64_t W, int connectivity);
 
 /* Label one H x W image (device pointers).  Allocates its workspace stream-
@@ -269,7 +271,9 @@ ccl_status_t ccl_label_host_async(const uint8_t* h_images, int64_t B, int64_t H,
  * Six launches per step: local = K1, K2, strip edges, strip reps; finalize =
  * slot union (a min-label union-find over the k*2W slots), K3.
  * Workspace: >= ccl_strip_workspace_bytes(rows, W, k, connectivity), the same
- * buffer for both calls.  Errors as above; CCL_ERR_DIMS also for rank/k/row0
+ * buffer for both calls (ccl_workspace_bytes of the strip plus 4 B per edge
+ * slot for the strip marks and 16 B per boundary slot for the slot
+ * union-find: about 4.5 B/px).  Errors as above; CCL_ERR_DIMS also for rank/k/row0
  * out of range. */
 size_t ccl_strip_workspace_bytes(int64_t rows, int64_t W, int k, int connectivity);
 ccl_status_t ccl_strip_local(const uint8_t* strip, int64_t rows, int64_t W, int64_t row0, int64_t H_total,

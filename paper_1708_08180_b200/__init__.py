@@ -28,6 +28,7 @@ from ._binding import (  # noqa: F401
     Workspace,
     boundary_work_items,
     default_tile_rows,
+    strip_workspace_bytes,
     label,
     raw,
     stage_fns,
@@ -36,5 +37,5 @@ from ._binding import (  # noqa: F401
     workspace_bytes,
 )
 
-__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "HostPipeline", "CCLError", "workspace_bytes", "boundary_work_items", "default_tile_rows",
+__all__ = ["label", "label_method", "label_equal", "label_3d", "component_stats", "STATS_FIELDS", "MethodWorkspace", "METHODS", "Workspace", "StripLabeler", "label_strips_emulated", "strip_bounds", "HostSession", "HostPipeline", "CCLError", "workspace_bytes", "boundary_work_items", "default_tile_rows", "strip_workspace_bytes",
            "stages", "stage_fns", "status_string", "raw"]

@@ -92,6 +92,10 @@ def workspace_bytes(B: int, H: int, W: int, connectivity: int = 8) -> int:
     return int(_lib.ccl_workspace_bytes(B, H, W, connectivity))
 
 
+def strip_workspace_bytes(rows: int, W: int, k: int, connectivity: int = 8) -> int:
+    return int(_lib.ccl_strip_workspace_bytes(rows, W, k, connectivity))
+
+
 def default_tile_rows(B: int, H: int, W: int) -> int:
     """The tile height tile_rows=0 selects for this geometry on the current device."""
     ty = _lib.ccl_default_tile_rows(B, H, W)

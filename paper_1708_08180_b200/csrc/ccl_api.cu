@@ -56,6 +56,7 @@ struct Plan {
     ccl::Geom g;
     int ty;
     size_t G_bytes, bits_bytes, runs_bytes, edge_bytes, F_bytes, defer_bytes, ready_bytes;
+    size_t strip_F_bytes;  // F (strip marks / resolved labels): strip stages only, else F_bytes = 0
     size_t total() const {
         return G_bytes + bits_bytes + runs_bytes + edge_bytes + F_bytes + defer_bytes + ready_bytes;
     }
@@ -123,7 +124,8 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
                                    tiles32 * ccl::edge_slots(32)});
     if (slots >= size_t(INT32_MAX)) return CCL_ERR_TOO_LARGE;
     p.G_bytes = align_up(slots * sizeof(uint64_t));
-    p.F_bytes = align_up(slots * sizeof(int32_t));
+    p.strip_F_bytes = align_up(slots * sizeof(int32_t));
+    p.F_bytes = 0;  // strip_plan / ccl_strip_workspace_bytes add it
     p.bits_bytes = align_up(size_t(B) * size_t(H) * size_t(p.g.WW) * sizeof(uint32_t));
     // per-run records: capacity of the worst case (alternating pixels) for the
     // tallest tile config, so the size does not depend on tile_rows
@@ -309,7 +311,11 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     const size_t smem = smem_bytes<TY>();
     // persistent K1/K3: one wave of resident blocks walks all tiles
     const unsigned grid1 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(1)));
+#ifdef CCL_K3_GRID  // timing experiments only (tools/build_variant.sh)
+    const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)CCL_K3_GRID));
+#else
     const unsigned grid3 = unsigned(std::min<long long>(ntiles, (long long)persistent_blocks<TY, CONN, VEC>(3)));
+#endif
     const long long n_h = (long long)g.B * (g.tiles_y - 1) * g.tiles_x;
     const long long n_v = (long long)g.B * ((g.tiles_y + ccl::v_bands<TY>() - 1) / ccl::v_bands<TY>()) *
                           (g.tiles_x - 1);
@@ -812,6 +818,7 @@ static size_t align_up_c(size_t v) { return (v + 255) / 256 * 256; }
 size_t ccl_strip_workspace_bytes(int64_t rows, int64_t W, int k, int connectivity) {
     Plan p;
     if (k < 1 || make_plan(1, rows, W, connectivity, 0, p) != CCL_OK) return 0;
+    p.F_bytes = p.strip_F_bytes;
     return p.total() + align_up_c(size_t(k) * 2 * size_t(W) * sizeof(uint64_t));
 }
 
@@ -825,6 +832,7 @@ static ccl_status_t strip_plan(int64_t rows, int64_t W, int64_t row0, int64_t H_
     if (st != CCL_OK) return st;
     p.g.label_off = int(row0 * W);
     p.g.strip = 1;
+    p.F_bytes = p.strip_F_bytes;
     p.g.force_top = row0 > 0;
     p.g.force_bottom = row0 + rows < H_total;
     return CCL_OK;

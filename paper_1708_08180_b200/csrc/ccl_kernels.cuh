@@ -1899,7 +1899,11 @@ template <bool RES>
 __device__ __forceinline__ void k3_resolve_tile(int32_t* slot, const Geom& g, const int32_t* E, uint64_t* G,
                                                 const StripFinal& sf, unsigned t, int first, int stride) {
     const int n = min(__ldcg(E + size_t(t) * kEdgeCap), kFlCap);
+#ifdef CCL_K3_NORES  // timing experiments only: no resolve (wrong labels)
+    for (int i = first; i < n; i += stride) slot[i] = i;
+#else
     for (int i = first; i < n; i += stride) slot[i] = edge_label<RES>(g, G, sf, t, i);
+#endif
 }
 
 #ifndef CCL_K3_COOP

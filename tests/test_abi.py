@@ -95,9 +95,16 @@ def test_workspace_bytes(ccl):
     assert ccl.workspace_bytes(1, 4, 4, 5) == 0
     H, W = 1080, 1920
     n = ccl.workspace_bytes(3, H, W, 8)
-    # parent array (int32 per pixel) + bit mask (one uint32 word per 32 px per row)
-    assert n >= 3 * H * W * 4 + 3 * H * ((W + 31) // 32) * 4
+    # bit mask (one uint32 word per 32 px per row) + run records (4 B per run,
+    # worst case 512 runs per 1024-px tile row, rows rounded up to 32)
+    bits = 3 * H * ((W + 31) // 32) * 4
+    records = 3 * ((W + 1023) // 1024) * ((H + 31) // 32 * 32) * 512 * 4
+    assert n >= bits + records
+    # compact: edge slots instead of a per-pixel parent array
+    assert n < 4.5 * 3 * H * W
     assert n % 256 == 0
+    # the strip stages add the strip marks and the boundary slot union-find
+    assert ccl.strip_workspace_bytes(H, W, 2, 8) > ccl.workspace_bytes(1, H, W, 8)
 
 
 def boundaries(n, t):

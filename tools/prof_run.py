@@ -17,6 +17,8 @@ ap.add_argument("--size", type=int, default=8192)
 ap.add_argument("--conn", type=int, default=8)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--tile-rows", type=int, default=0)
+ap.add_argument("--evict", action="store_true",
+                help="read 512 MiB after the step: that read kernel's DRAM writes are the step's dirty L2 lines")
 a = ap.parse_args()
 H = W = a.size
 if a.kind == "texture":
@@ -31,8 +33,11 @@ t = torch.from_numpy(img).cuda()
 ws = ccl.Workspace(1, H, W, a.conn)
 out = torch.empty((H, W), dtype=torch.int32, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush.fill_(1)
 for _ in range(a.iters):
-    flush.zero_()
+    flush.sum(dtype=torch.int64)  # read-only L2 flush: nothing of the earlier work stays in L2
     ccl.label(t, a.conn, out=out, workspace=ws, tile_rows=a.tile_rows)
+    if a.evict:
+        flush.sum(dtype=torch.int64)  # write-back of the step's dirty lines happens here
 torch.cuda.synchronize()
 print("ok", int(out.max().item()))
