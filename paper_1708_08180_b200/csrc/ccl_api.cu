@@ -342,13 +342,17 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
             // few boundaries (small images): split each horizontal one over
             // 2 or 4 warps so the launch still fills the GPU (one task per
             // warp, ~5900 warps resident in one wave)
-            int sub_log2 = 0;
+#ifndef CCL_K2_SUB_MIN
+#define CCL_K2_SUB_MIN 0  // minimum split of a horizontal boundary: 2^SUB_MIN warps
+#endif
+            int sub_log2 = CCL_K2_SUB_MIN;
             while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= (long long)sm_count() * 40) ++sub_log2;
 #ifndef CCL_K2_DBG
 #define CCL_K2_DBG 0  // timing experiments only (tools/build_variant.sh): 3 = skip K2, 4 = no unions
 #endif
             e = launch_pdl(ccl::k_boundary<TY, CONN, CCL_K2_DBG>,
-                           unsigned(((n_h << sub_log2) + n_v + 7) / 8), 256, 0, s, g,
+                           unsigned(((n_h << sub_log2) + n_v + ccl::kK2Warps - 1) / ccl::kK2Warps),
+                           32 * ccl::kK2Warps, 0, s, g,
                            (const uint32_t*)bits, (const uint32_t*)runs, (const int32_t*)E, G, n_h, n_v, sub_log2);
             if (e != cudaSuccess) return e;
         }
@@ -516,6 +520,28 @@ ccl_status_t label_alloc(const uint8_t* images, int64_t B, int64_t H, int64_t W,
 }  // namespace
 
 extern "C" {
+
+#ifdef CCL_TIMELINE  // profiling builds only (not declared in include/ccl.h)
+int ccl_debug_timeline(unsigned long long* out, int reset) {
+    if (out && cudaMemcpyFromSymbol(out, ccl::g_tl, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long init[8];
+        for (int i = 0; i < 8; ++i) init[i] = (i == 0 || i == 2 || i == 4 || i == 5) ? ~0ull : 0ull;
+        if (cudaMemcpyToSymbol(ccl::g_tl, init, sizeof(init)) != cudaSuccess) return -1;
+    }
+    return 0;
+}
+#ifdef CCL_STATS
+// per-K2-task counters (union steps, find hops, link retries, rounds) into a caller device buffer
+int ccl_debug_k2_taskstat(unsigned* dev_buf) {
+    return cudaMemcpyToSymbol(ccl::g_k2_taskstat, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
+// per-K2-task globaltimer (start, end) pairs into a caller device buffer (DBG 8 builds)
+int ccl_debug_k2_stamps(unsigned long long* dev_buf) {
+    return cudaMemcpyToSymbol(ccl::g_k2_stamps, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 const char* ccl_status_string(ccl_status_t status) {
     switch (status) {

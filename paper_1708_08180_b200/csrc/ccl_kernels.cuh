@@ -84,8 +84,17 @@ __host__ __device__ constexpr int k1_warps() { return k1_threads<TY>() / 32; }
 #endif
 __host__ __device__ constexpr int k1_cap32() {
     // 16 KB of row words; 512 threads: 11776 runs (110 KB, 2 blocks per SM);
-    // 256 threads: 4800 runs at 4 blocks per SM (54 KB), 3456 at 5 (44 KB)
-    return CCL_K1_T32 == 512 ? 11776 : (CCL_K1_BLOCKS32 == 4 ? 4800 : 3456);
+    // 256 threads: 4800 runs at 4 blocks per SM (54 KB), 3456 at 5 (44 KB),
+    // 2400 at 6 (36 KB).  Measured (C3, 32-row tiles, µs/step): 6 vs 5 blocks
+    // texture 103.1 vs 103.3, C4 3190 vs 3242, noise 694 vs 734, percolation
+    // 673 vs 675, but the smaller cap raises the worst-case edge slots per
+    // tile (9 row ranges instead of 6): workspace 4.5 instead of 3.7 B/px;
+    // 4 blocks: texture 105.4.  5 kept.
+#ifdef CCL_K1_CAP32
+    return CCL_K1_CAP32;
+#else
+    return CCL_K1_T32 == 512 ? 11776 : (CCL_K1_BLOCKS32 == 4 ? 4800 : (CCL_K1_BLOCKS32 == 6 ? 2400 : 3456));
+#endif
 }
 __host__ __device__ constexpr int k1_cap_n(int TY) {
     return TY * kTileW / 2 < (TY > 16 ? k1_cap32() : CCL_K1_CAP16) ? TY * kTileW / 2
@@ -98,6 +107,10 @@ __host__ __device__ constexpr int k1_cap() { return k1_cap_n(TY); }
 __host__ __device__ constexpr int k1_max_ranges(int TY) {
     return TY * kTileW / 2 <= k1_cap_n(TY) ? 1 : 1 + (TY * kTileW / 2) / (k1_cap_n(TY) - kTileW / 2 + 1);
 }
+#ifndef CCL_K2_WARPS
+#define CCL_K2_WARPS 8  // warps (boundary tasks) per K2 block
+#endif
+constexpr int kK2Warps = CCL_K2_WARPS;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kTag = int(0x80000000u);
 
@@ -336,7 +349,7 @@ __device__ unsigned long long g_stat_unions = 0, g_stat_steps = 0, g_stat_finds 
 // retries, [3] rounds (task = blockIdx.x * 8 + warp)
 __device__ unsigned* g_k2_taskstat = nullptr;
 #define CCL_STAT(v) atomicAdd(&(v), 1ull)
-#define CCL_TASKSTAT(k, n) (g_k2_taskstat ? (void)atomicAdd(g_k2_taskstat + 4 * (blockIdx.x * 8u + (threadIdx.x >> 5)) + (k), (n)) : (void)0)
+#define CCL_TASKSTAT(k, n) (g_k2_taskstat ? (void)atomicAdd(g_k2_taskstat + 4 * (blockIdx.x * unsigned(CCL_K2_WARPS) + (threadIdx.x >> 5)) + (k), (n)) : (void)0)
 #else
 #define CCL_STAT(v) ((void)0)
 #define CCL_TASKSTAT(k, n) ((void)0)
@@ -717,6 +730,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Timeline of one fused step (profiling builds only, -DCCL_TIMELINE; read by
+// ccl_debug_timeline): globaltimer ns of 0 K1 first block start, 1 K1 last
+// block end, 2 K2 first task start, 3 K2 last task end, 4 K3 first block
+// start, 5 K3 first block past its PDL wait, 6 K3 last block end, 7 K1 last
+// tile published.
+#ifdef CCL_TIMELINE
+__device__ unsigned long long g_tl[8];
+#define CCL_TL_MIN(i) atomicMin(&g_tl[i], gtimer())
+#define CCL_TL_MAX(i) atomicMax(&g_tl[i], gtimer())
+#else
+#define CCL_TL_MIN(i) ((void)0)
+#define CCL_TL_MAX(i) ((void)0)
+#endif
 __device__ __forceinline__ void k1_stamp(unsigned t, int k) {
     if (g_k1_stamps) g_k1_stamps[size_t(t) * 8 + k] = clock64();
 }
@@ -1150,10 +1176,11 @@ __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, cons
     // block's next tile, in flight during the rest of this one ...
     if (!INPLACE && VEC && tnext < ntiles) k1_prefetch<TY>(img, g, tnext, warp, lane, v8, cur);
     // ... and its other rows are pulled into L2 with bulk prefetches
+    constexpr int L2R = k1_pf_rows<TY>() * k1_warps<TY>();  // first row pulled into L2
     if (!INPLACE && VEC && RPW > k1_pf_rows<TY>() && tnext < ntiles && warp == k1_warps<TY>() - 1 &&
-        lane < TY - k1_pf_rows<TY>() * k1_warps<TY>()) {
+        lane < TY - L2R) {
         const TileId nx = decode_tile<TY>(g, tnext);
-        const int y = nx.y0 + k1_pf_rows<TY>() * k1_warps<TY>() + lane;
+        const int y = nx.y0 + L2R + lane;
         if (y < g.H) {
             const uint8_t* row = img + size_t(nx.b) * size_t(g.npx) + size_t(y) * size_t(g.W) + nx.x0;
             const unsigned bytes = unsigned(min(kTileW, g.W - nx.x0));
@@ -1185,6 +1212,7 @@ __device__ __forceinline__ void k1_publish(const Geom& g, unsigned t) {
         if (threadIdx.x == 0) {
             __threadfence();
             st_release_u64(g.ready + t, g.epoch);
+            CCL_TL_MAX(7);
         }
     }
 }
@@ -1296,7 +1324,7 @@ __device__ __forceinline__ void boundary_h(const Geom& g, const uint32_t* bits, 
     s_w[1][lane] = Word{up, su, 0, iu - __popc(su)};
     __syncwarp();
 #ifdef CCL_K2_PHASES  // profiling harness only (tools/k1_phases.cu)
-    const unsigned ptask = blockIdx.x * 8u + (threadIdx.x >> 5);
+    const unsigned ptask = blockIdx.x * unsigned(CCL_K2_WARPS) + (threadIdx.x >> 5);
     if (g_k2_phase && lane == 0) g_k2_phase[4 * size_t(ptask)] = gtimer();
 #endif
     const uint32_t o = cur & up, oL = curL & upL;
@@ -1432,17 +1460,21 @@ __device__ __forceinline__ void boundary_v(const Geom& g, const int32_t* E, uint
 // K2 boundary analysis: one warp per horizontal tile boundary (1024 px) or per
 // 32-row stretch of a vertical one; tasks are independent (lock-free unions).
 template <int TY, int CONN, int DBG = 0>
-__global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __restrict__ bits,
+#ifndef CCL_K2_MINB
+#define CCL_K2_MINB 1  // min resident K2 blocks per SM (register cap: 65536 / (MINB * 32 * warps))
+#endif
+__global__ void __launch_bounds__(32 * kK2Warps, CCL_K2_MINB) k_boundary(Geom g, const uint32_t* __restrict__ bits,
                                                   const uint32_t* __restrict__ R,
                                                   const int32_t* __restrict__ E,
                                                   uint64_t* __restrict__ G, long long n_h, long long n_v,
                                                   int sub_log2 = 0) {
-    __shared__ Word s_w[8][2][kWords];
-    __shared__ int2 s_pairs[8][32 * kPairsPerLane];
+    __shared__ Word s_w[kK2Warps][2][kWords];
+    __shared__ int2 s_pairs[kK2Warps][32 * kPairsPerLane];
     if (!g.epoch) pdl_wait();  // else: each task waits for its own tiles' ready flags
     const int warp = threadIdx.x >> 5;
     // (task counts are < 2^31: <= 2 per 16 x 1024 tile; 32-bit index math)
-    const unsigned task = blockIdx.x * 8u + unsigned(warp);
+    const unsigned task = blockIdx.x * unsigned(kK2Warps) + unsigned(warp);
+    if ((threadIdx.x & 31) == 0) CCL_TL_MIN(2);
     const unsigned long long t_start = (DBG & 8) ? gtimer() : 0ull;
     const unsigned nh_sub = unsigned(n_h) << sub_log2;  // horizontal boundaries, split in 2^sub_log2 warps each
     if (task < nh_sub) {
@@ -1480,6 +1512,7 @@ __global__ void __launch_bounds__(256) k_boundary(Geom g, const uint32_t* __rest
         }
         boundary_v<TY, CONN>(g, E, G, b, band0, bx);
     }
+    if ((threadIdx.x & 31) == 0) CCL_TL_MAX(3);
     if ((DBG & 8) && (threadIdx.x & 31) == 0 && g_k2_stamps && task < nh_sub + unsigned(n_v)) {
         g_k2_stamps[2 * size_t(task)] = t_start;
         g_k2_stamps[2 * size_t(task) + 1] = gtimer();
@@ -1509,6 +1542,7 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     // be scheduled onto the SM slots K1's finished blocks free (its tasks wait
     // on the per-tile ready flags)
     if (g.epoch) pdl_launch_dependents();
+    if (threadIdx.x == 0) CCL_TL_MIN(0);
     if (t >= ntiles) return;
     constexpr bool PF = VEC;  // the first tile's register rows (k1_pf_rows)
     // one register set: loaded with tile t before the loop, then refilled with
@@ -1523,13 +1557,14 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     // machinery stays out of this loop's code and registers
     while (t < ntiles) {
         const int v = k1_masks<TY, CONN, VEC, false, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, warp, lane, v8);
-        if (__shfl_sync(kFull, v, TY - 1) <= k1_cap<TY>()) {  // block-uniform
+        const bool fits = __shfl_sync(kFull, v, TY - 1) <= k1_cap<TY>();  // block-uniform
+        if (fits) {
             k1_range<TY, CONN, DBG, true>(sm, g, t, decode_tile<TY>(g, t), v, 0, TY, 0, G, R, E, F, warp, lane);
-            k1_publish(g, t);
         } else if (threadIdx.x == 0) {
             // (block b's list: g.defer[b * per ..], per = ceil(ntiles / grid) slots)
             g.defer[size_t(blockIdx.x) * ((ntiles + gridDim.x - 1) / gridDim.x) + sm.ndefer++] = t;
         }
+        if (fits) k1_publish(g, t);
         t += gridDim.x;
     }
     __syncthreads();
@@ -1540,6 +1575,7 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
         k1_dense<TY, CONN, DBG>(sm, g, td, v, G, R, E, F, warp, lane);
         __syncthreads();  // smem is reused by the next deferred tile
     }
+    if (threadIdx.x == 0) CCL_TL_MAX(1);
 }
 
 // ------------------------------------------- K2 tail: resolve edge roots
@@ -1943,6 +1979,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     LinkSmem<TY>& sm = *reinterpret_cast<LinkSmem<TY>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) CCL_TL_MIN(4);
     if (threadIdx.x == 0) {
         sm.produced = 0;
         sm.consumed = 0;
@@ -1960,6 +1997,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
     }
     pdl_wait();
+    if (threadIdx.x == 0) CCL_TL_MIN(5);
     if (warp < kWarps && !g.k3_early) {  // K3 right after K1 (no boundaries): K1's outputs only after the wait
         k3_prefetch<TY>(bits, R, g, t, warp, lane, a);
         if (t + gridDim.x < ntiles) k3_prefetch<TY>(bits, R, g, t + gridDim.x, warp, lane, b);
@@ -1990,6 +2028,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) k_link(Geom g, const uint32_t* 
         if (t >= ntiles) break;
     }
     if (TMA && lane == 0) tma_wait_all();  // smem must outlive the bulk stores
+    if (threadIdx.x == 0) CCL_TL_MAX(6);
 }
 
 }  // namespace ccl
