@@ -537,6 +537,10 @@ int ccl_debug_k2_taskstat(unsigned* dev_buf) {
     return cudaMemcpyToSymbol(ccl::g_k2_taskstat, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? 0 : -1;
 }
 #endif
+// per-tile publish times (globaltimer) into a caller device buffer
+int ccl_debug_tile_pub(unsigned long long* dev_buf) {
+    return cudaMemcpyToSymbol(ccl::g_tile_pub, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? 0 : -1;
+}
 // per-K2-task globaltimer (start, end) pairs into a caller device buffer (DBG 8 builds)
 int ccl_debug_k2_stamps(unsigned long long* dev_buf) {
     return cudaMemcpyToSymbol(ccl::g_k2_stamps, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? 0 : -1;

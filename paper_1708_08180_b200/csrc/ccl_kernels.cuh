@@ -737,6 +737,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // tile published.
 #ifdef CCL_TIMELINE
 __device__ unsigned long long g_tl[8];
+__device__ unsigned long long* g_tile_pub = nullptr;  // per tile: globaltimer at its publish
 #define CCL_TL_MIN(i) atomicMin(&g_tl[i], gtimer())
 #define CCL_TL_MAX(i) atomicMax(&g_tl[i], gtimer())
 #else
@@ -1213,6 +1214,9 @@ __device__ __forceinline__ void k1_publish(const Geom& g, unsigned t) {
             __threadfence();
             st_release_u64(g.ready + t, g.epoch);
             CCL_TL_MAX(7);
+#ifdef CCL_TIMELINE
+            if (g_tile_pub) g_tile_pub[t] = gtimer();
+#endif
         }
     }
 }

@@ -98,3 +98,24 @@ if hasattr(lib, "ccl_debug_k2_stamps") and os.environ.get("K2STAMPS"):
               [round(float(np.percentile(sp[late], q)), 2) for q in (50, 90, 100)] if late.any() else None)
     top = np.argsort(-(a[:, 1] - a[:, 0]) * used)[:8]
     print("longest tasks (id, start, end us):", [(int(i), round((a[i, 0] - t0) / 1e3, 1), round((a[i, 1] - t0) / 1e3, 1)) for i in top])
+
+# per-tile publish times: K1's rounds (tile t is round t // grid of the persistent grid)
+if hasattr(lib, "ccl_debug_tile_pub") and os.environ.get("TILEPUB"):
+    import numpy as np
+    ntiles = (H // 32) * (W // 1024)
+    tp = torch.zeros(ntiles, dtype=torch.int64, device="cuda")
+    lib.ccl_debug_tile_pub.argtypes = [ctypes.c_void_p]
+    lib.ccl_debug_tile_pub(tp.data_ptr())
+    flush.zero_()
+    torch.cuda.synchronize()
+    fn(None, 1)
+    ccl.label(img, 8, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    fn(buf, 0)
+    lib.ccl_debug_tile_pub(None)
+    pub = (tp.cpu().numpy().astype("float64") - float(buf[0])) / 1e3
+    grid = int(os.environ.get("K1GRID", 740))
+    for r in range((ntiles + grid - 1) // grid):
+        x = pub[r * grid:(r + 1) * grid]
+        print(f"K1 round {r}: {len(x)} tiles published p10 {np.percentile(x, 10):.1f} p50 {np.percentile(x, 50):.1f} "
+              f"p90 {np.percentile(x, 90):.1f} max {x.max():.1f} us")
