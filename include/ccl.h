@@ -55,7 +55,7 @@ typedef enum {
     CCL_ERR_ALIAS = 5,         /* input and output / workspace byte ranges overlap   */
     CCL_ERR_WORKSPACE = 6,     /* workspace smaller than ccl_workspace_bytes()       */
     CCL_ERR_CUDA = 7,          /* a CUDA runtime call or launch failed               */
-    CCL_ERR_CONFIG = 8         /* unsupported tile configuration                     */
+    CCL_ERR_CONFIG = 8         /* unsupported tile configuration / threshold         */
 } ccl_status_t;
 
 /* Human-readable text for a status code (static storage, never NULL). */
@@ -109,6 +109,18 @@ ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64
                                          int connectivity, int32_t* labels_out,
                                          void* workspace, size_t workspace_bytes,
                                          int tile_rows, void* stream);
+
+/* As ccl_label_batched_cfg_async on grey-level images, with the binarisation
+ * fused into K1's load ("binarize": output 255 if input >=
+ * threshold; the paper thresholds its grey test images):
+ * a pixel is foreground iff its value >= threshold.  threshold = 1 is the
+ * default "nonzero" test; 0 makes every pixel foreground.  The labels are
+ * those of ccl_label on the binarised image.  threshold outside 0..255 ->
+ * CCL_ERR_CONFIG (nothing launched); other errors as above. */
+ccl_status_t ccl_label_threshold_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                       int connectivity, int threshold, int32_t* labels_out,
+                                       void* workspace, size_t workspace_bytes, int tile_rows,
+                                       void* stream);
 
 /* The three stages individually (same arguments as ccl_label_batched_cfg_async),
  * for per-kernel timing and stage tests.  They must be enqueued in this order on

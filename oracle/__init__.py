@@ -17,6 +17,8 @@ Contents
                         value" adjacency, every pixel labeled with its
                         component's 0-based minimum raster index.
 * ``label_3d``       -- 3D volumes (NEXT-4): C flood fill, 6- / 26-connectivity.
+* ``binarize``       -- SPEC.md:50-58 threshold (>= t -> 255), for the fused
+                        threshold-on-load mode.
 * ``relabel_compact`` -- the 1..K renumbering of a canonical label map
                         (SPEC.md:336): k for the k-th distinct label in
                         increasing order, 0 for background.
@@ -262,3 +264,13 @@ def relabel_compact(labels) -> np.ndarray:
         _, inv = np.unique(L[fg], return_inverse=True)
         out[fg] = (inv + 1).astype(np.int32)
     return out
+
+
+def binarize(img, threshold: int) -> np.ndarray:
+    """SPEC.md:50-58 binarize: 255 where the input >= threshold, else 0
+    (dimensions preserved).  The CUDA path fuses this test into K1's load
+    (ccl_label_threshold_async); its labels must equal label_bfs(binarize(img, t))."""
+    a = np.asarray(img)
+    if a.dtype != np.uint8:
+        raise ValueError("expected uint8")
+    return np.where(a >= int(threshold), np.uint8(255), np.uint8(0))

@@ -35,6 +35,7 @@ SIGNATURES = {
     "ccl_stage_boundary": (_int, [_i64, _i64, _i64, _int, _vp, _sz, _int, _vp]),
     "ccl_stage_link": (_int, [_i64, _i64, _i64, _int, _vp, _vp, _sz, _int, _vp]),
     "ccl_default_tile_rows": (_int, [_i64, _i64, _i64]),
+    "ccl_label_threshold_async": (_int, [_vp, _i64, _i64, _i64, _int, _int, _vp, _vp, _sz, _int, _vp]),
     "ccl_boundary_work_items": (_i64, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "ccl_host_scratch_bytes": (_sz, [_i64, _i64, _i64, _int]),
     "ccl_label_host_async": (_int, [_vp, _i64, _i64, _i64, _int, _vp, _vp, _sz, _vp]),
@@ -188,10 +189,12 @@ class Workspace:
 
 
 def label(image, connectivity: int = 8, *, out=None, workspace: Workspace | None = None,
-          tile_rows: int = 0, stream=None):
+          tile_rows: int = 0, stream=None, threshold: int = 1):
     """Label a uint8 CUDA image [H,W] or batch [B,H,W]; returns int32 labels of
     the same shape (0 = background, 1 + min raster index per component, per
-    image).  Enqueued on ``stream`` (default: torch's current stream)."""
+    image).  Foreground: value >= ``threshold`` (default 1: nonzero; another
+    value runs ccl_label_threshold_async, the binarisation fused into K1).
+    Enqueued on ``stream`` (default: torch's current stream)."""
     torch = _torch()
     _check_image(image)
     B, H, W = _shape3(image)
@@ -205,9 +208,15 @@ def label(image, connectivity: int = 8, *, out=None, workspace: Workspace | None
         if workspace is None:
             workspace = Workspace(B, H, W, connectivity, device=image.device)
         _same_device(image.device, workspace.buf)
-        _check(_lib.ccl_label_batched_cfg_async(
-            ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
-            workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(s)), "ccl_label_batched_cfg_async")
+        if threshold == 1:
+            _check(_lib.ccl_label_batched_cfg_async(
+                ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), ctypes.c_void_p(out.data_ptr()),
+                workspace.ptr(), workspace.nbytes, int(tile_rows), _stream_ptr(s)), "ccl_label_batched_cfg_async")
+        else:
+            _check(_lib.ccl_label_threshold_async(
+                ctypes.c_void_p(image.data_ptr()), B, H, W, int(connectivity), int(threshold),
+                ctypes.c_void_p(out.data_ptr()), workspace.ptr(), workspace.nbytes, int(tile_rows),
+                _stream_ptr(s)), "ccl_label_threshold_async")
     return out
 
 

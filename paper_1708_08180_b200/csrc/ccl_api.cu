@@ -113,6 +113,8 @@ ccl_status_t make_plan(int64_t B, int64_t H, int64_t W, int conn, int tile_rows,
     p.g.epoch = 0;
     p.g.ready = nullptr;
     p.g.defer = nullptr;
+    p.g.thr = 1;  // foreground = nonzero (ccl_label_threshold_async sets another threshold)
+    p.g.thr_k = 0x7F7F7F7Fu;
     p.g.ntiles = unsigned(int64_t(B) * p.g.tiles_x * p.g.tiles_y);
     // edge slots (the boundary analysis' union-find nodes, 8 B each) and their
     // resolved labels in strip mode (4 B each): edge_slots(TY) per tile, sized
@@ -177,6 +179,12 @@ cudaError_t setup_attrs_now() {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem_bytes_k1<TY>()));
     if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem_bytes_k1<TY>()))) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(ccl::k_local_merge<TY, CONN, VEC, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem_bytes_k1<TY>()))) != cudaSuccess)
+        return e;
     const int sm3 = int(smem_bytes<TY>());
     if ((e = cudaFuncSetAttribute(k3_kernel<TY, CONN, VEC, false, true>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sm3)) != cudaSuccess)
@@ -331,8 +339,10 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
     }
     g.defer = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + p.total() - p.ready_bytes - p.defer_bytes);
     if (stages & kK1) {
-        ccl::k_local_merge<TY, CONN, VEC><<<grid1, ccl::k1_threads<TY>(), smem_bytes_k1<TY>(), s>>>(
-            img, g, bits, G, runs, E, F, unsigned(ntiles));
+        // the foreground test: nonzero, or value >= thr (fused threshold, THR 1 / 2)
+        auto k1 = g.thr == 1 ? ccl::k_local_merge<TY, CONN, VEC>
+                             : (g.thr <= 128 ? ccl::k_local_merge<TY, CONN, VEC, 0, 1> : ccl::k_local_merge<TY, CONN, VEC, 0, 2>);
+        k1<<<grid1, ccl::k1_threads<TY>(), smem_bytes_k1<TY>(), s>>>(img, g, bits, G, runs, E, F, unsigned(ntiles));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (stages & kK2) {
@@ -589,6 +599,21 @@ ccl_status_t ccl_label_batched_cfg_async(const uint8_t* images, int64_t B, int64
     if (B == 0) return CCL_OK;
     st = validate_buffers(p, images, labels_out, workspace, workspace_bytes, kAll);
     if (st != CCL_OK) return st;
+    return run(p, connectivity, kAll, images, labels_out, workspace, static_cast<cudaStream_t>(stream));
+}
+
+ccl_status_t ccl_label_threshold_async(const uint8_t* images, int64_t B, int64_t H, int64_t W,
+                                       int connectivity, int threshold, int32_t* labels_out, void* workspace,
+                                       size_t workspace_bytes, int tile_rows, void* stream) {
+    if (threshold < 0 || threshold > 255) return CCL_ERR_CONFIG;
+    Plan p;
+    ccl_status_t st = make_plan(B, H, W, connectivity, tile_rows, p);
+    if (st != CCL_OK) return st;
+    if (B == 0) return CCL_OK;
+    st = validate_buffers(p, images, labels_out, workspace, workspace_bytes, kAll);
+    if (st != CCL_OK) return st;
+    p.g.thr = threshold;
+    p.g.thr_k = (threshold <= 128 ? uint32_t(128 - threshold) : uint32_t(256 - threshold)) * 0x01010101u;
     return run(p, connectivity, kAll, images, labels_out, workspace, static_cast<cudaStream_t>(stream));
 }
 

@@ -140,6 +140,10 @@ struct Geom {
     int label_off;     // added to every label (row0 * W_total: labels are global)
     int force_top;     // the image's first row borders another strip
     int force_bottom;  // the image's last row borders another strip
+    // foreground test fused into K1's load (ccl_label_threshold_async):
+    // value >= thr; thr_k = the SWAR constant of nzc4 (K1 template THR 1 / 2)
+    int thr;
+    uint32_t thr_k;
     int k3_early;      // K3 may read K1's outputs before its PDL wait (K1 finished before K3's predecessor)
     unsigned ntiles;   // tiles of the whole batch: the stride of the edge-slot numbering
     int strip;         // strip mode (row-strip sharding): K1 also clears the strip marks F of its edge slots
@@ -218,6 +222,26 @@ __device__ __forceinline__ uint32_t nz16(uint4 v) {
     r = (r << 4) + nz4(v.z);
     r = (r << 4) + nz4(v.y);
     return (r << 4) + nz4(v.x);
+}
+
+// Thresholded variant (value >= c, SPEC.md:50-58 binarize): for c <= 128 a
+// byte b passes iff (b & 0x7F) + (128 - c) reaches bit 7 or b >= 128 (THR 1,
+// k = (128 - c) x 0x01010101; c = 1 is nz4); for c > 128 iff b >= 128 and
+// (b & 0x7F) + (256 - c) reaches bit 7 (THR 2, k = (256 - c) x 0x01010101).
+// No carry crosses a byte (each sum < 256).
+template <int THR>
+__device__ __forceinline__ uint32_t nzc4(uint32_t w, uint32_t k) {
+    const uint32_t x = (w & 0x7F7F7F7Fu) + k;
+    const uint32_t t = (THR == 2 ? (x & w) : (x | w)) & 0x80808080u;
+    return (t * 0x00204081u) >> 28;
+}
+template <int THR>
+__device__ __forceinline__ uint32_t nzc16(uint4 v, uint32_t k) {
+    if (THR == 0) return nz16(v);
+    uint32_t r = nzc4<THR>(v.w, k);
+    r = (r << 4) + nzc4<THR>(v.z, k);
+    r = (r << 4) + nzc4<THR>(v.y, k);
+    return (r << 4) + nzc4<THR>(v.x, k);
 }
 
 // Programmatic dependent launch (K2, resolve and K3 are launched with the
@@ -1124,7 +1148,7 @@ __device__ __forceinline__ void k1_internal_boundary(K1Smem<TY>& sm, const Geom&
 // the tile's pixels are loaded here (run-dense tiles, processed after the
 // block's other tiles); else they were prefetched into cur, which then
 // receives the next tile.
-template <int TY, int CONN, bool VEC, bool INPLACE, int DBG = 0>
+template <int TY, int CONN, bool VEC, bool INPLACE, int DBG = 0, int THR = 0>
 __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, const Geom& g, unsigned t,
                                         ImgRegs<TY>& cur, unsigned tnext, unsigned ntiles, uint32_t* bits,
                                         int warp, int lane, bool v8) {
@@ -1158,13 +1182,13 @@ __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, cons
             // the lane's own 32 contiguous pixels: no cross-lane assembly
             const uint4 v0 = i < PFR ? cur.v[i < PFR ? i : 0][0] : lv[i >= PFR ? i - PFR : 0][0];
             const uint4 v1 = i < PFR ? cur.v[i < PFR ? i : 0][1] : lv[i >= PFR ? i - PFR : 0][1];
-            m = nz16(v0) | (nz16(v1) << 16);
+            m = nzc16<THR>(v0, g.thr_k) | (nzc16<THR>(v1, g.thr_k) << 16);
         } else {
             const uint8_t* row = im + size_t(y < g.H ? y : 0) * size_t(g.W);
 #pragma unroll 4
             for (int k = 0; k < kWords; ++k) {
                 const int x = id.x0 + (k << 5) + lane;
-                const bool fg = (y < g.H && x < g.W) ? (row[x] != 0) : false;
+                const bool fg = (y < g.H && x < g.W) ? (THR ? int(row[x]) >= g.thr : row[x] != 0) : false;
                 const uint32_t bal = __ballot_sync(kFull, fg);
                 if (lane == k) m = bal;
             }
@@ -1530,7 +1554,7 @@ __global__ void __launch_bounds__(32 * kK2Warps, CCL_K2_MINB) k_boundary(Geom g,
 // (Fusing the boundary unions into this kernel -- each boundary merged by the
 // block that publishes its second tile -- measured 4x slower: the blocks
 // stall on the unions' global latency.)
-template <int TY, int CONN, bool VEC, int DBG = 0>
+template <int TY, int CONN, bool VEC, int DBG = 0, int THR = 0>
 __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local_merge(const uint8_t* __restrict__ img, Geom g,
                                                              uint32_t* __restrict__ bits,
                                                              uint64_t* __restrict__ G,
@@ -1560,7 +1584,7 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     // range; run-dense tiles are deferred to the loop below, so the range
     // machinery stays out of this loop's code and registers
     while (t < ntiles) {
-        const int v = k1_masks<TY, CONN, VEC, false, DBG>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, warp, lane, v8);
+        const int v = k1_masks<TY, CONN, VEC, false, DBG, THR>(sm, img, g, t, a, t + gridDim.x, ntiles, bits, warp, lane, v8);
         const bool fits = __shfl_sync(kFull, v, TY - 1) <= k1_cap<TY>();  // block-uniform
         if (fits) {
             k1_range<TY, CONN, DBG, true>(sm, g, t, decode_tile<TY>(g, t), v, 0, TY, 0, G, R, E, F, warp, lane);
@@ -1575,7 +1599,7 @@ __global__ void __launch_bounds__(k1_threads<TY>(), k1_min_blocks<TY>()) k_local
     const int nd = sm.ndefer;
     for (int i = 0; i < nd; ++i) {
         const unsigned td = unsigned(__ldcg(g.defer + size_t(blockIdx.x) * ((ntiles + gridDim.x - 1) / gridDim.x) + i));
-        const int v = k1_masks<TY, CONN, VEC, true, DBG>(sm, img, g, td, a, ntiles, ntiles, bits, warp, lane, v8);
+        const int v = k1_masks<TY, CONN, VEC, true, DBG, THR>(sm, img, g, td, a, ntiles, ntiles, bits, warp, lane, v8);
         k1_dense<TY, CONN, DBG>(sm, g, td, v, G, R, E, F, warp, lane);
         __syncthreads();  // smem is reused by the next deferred tile
     }

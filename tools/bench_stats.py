@@ -32,3 +32,15 @@ ms = statistics.median(ts)
 print(json.dumps({"what": "component_stats C3 8192x8192 texture labels", "components": int(counts[0]),
                   "ms_median": round(ms, 4), "gpx_s": round(n * n / ms / 1e6, 1),
                   "GB_s_at_4B_px": round(4 * n * n / ms / 1e6, 1)}))
+ts = []
+for _ in range(30):
+    flush.zero_()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    counts, _, rl = ccl.component_stats(L, 1 << 20, relabel=True)
+    b.record()
+    torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b))
+ms = statistics.median(ts)
+print(json.dumps({"what": "component_stats + 1..K relabel map, C3 8192x8192 texture labels",
+                  "ms_median": round(ms, 4), "GB_s_at_8B_px": round(8 * n * n / ms / 1e6, 1)}))
