@@ -658,6 +658,9 @@ struct __align__(16) WordE {
 #ifndef CCL_K1_CAP16
 #define CCL_K1_CAP16 4576
 #endif
+#ifndef CCL_K1_STEAL
+#define CCL_K1_STEAL 1  // union phase: runs beyond the first T1 in dynamic chunks of 32 per warp
+#endif
 #ifndef CCL_K1_UF2
 #define CCL_K1_UF2 0  // two-step local UF (up-link forest, then the remaining pairs)
 #endif
@@ -680,6 +683,7 @@ struct K1Smem {
     int32_t rcnt[TY];              // runs per row
     int32_t rbase[TY + 1];         // first run id of each row (exclusive prefix)
     int32_t ndefer;                // run-dense tiles of this block (listed in g.defer), labelled last
+    int32_t unext;                 // union phase: next unclaimed chunk of 32 runs (CCL_K1_STEAL)
 };
 
 // find / merge of §2.1.3 over tile run ids.
@@ -900,7 +904,10 @@ __device__ __forceinline__ int k1_range(K1Smem<TY>& sm, const Geom& g, unsigned 
             re[ke++] = uint16_t(xb + bit);
         }
     }
-    if (tid == 0) rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
+    if (tid == 0) {
+        rs[total] = uint16_t(63 << 10);  // no run of any row: ends every neighbour search
+        sm.unext = T1;  // dynamic union chunks start after the static first pass
+    }
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 2);
     if (DBG & 1) {
@@ -950,13 +957,13 @@ __device__ __forceinline__ int k1_range(K1Smem<TY>& sm, const Geom& g, unsigned 
             k1_union<DBG>(P, jd, k);
     }
 #else
-#pragma unroll 1
-    for (int k = tid; k < total; k += T1) {
+    // run k's two unions: the first runs of rows r-1 and r+1 touching its
+    // contact interval [p, q] (both searches are issued before either union:
+    // the phase is bound by this chain)
+    auto run_unions = [&](int k) {
         const int rsk = rs[k];
         const int r = rsk >> 10, si = rsk & 1023, ei = re[k];
         const int p = max(si - D, 0), q = min(ei + D, kTileW - 1);
-        // first runs of rows r-1 and r+1 touching [p, q] (both searches are
-        // issued before either union: the phase is bound by this chain)
         const WordE uu = sm.wd[r > r0 ? r - 1 : r0][p >> 5];
         const WordE ud = sm.wd[r + 1 < r1 ? r + 1 : r1 - 1][p >> 5];
         const uint32_t below = (1u << (p & 31)) - 1u;
@@ -965,7 +972,27 @@ __device__ __forceinline__ int k1_range(K1Smem<TY>& sm, const Geom& g, unsigned 
         const int rsu = rs[ju], rsd = rs[jd];  // may be another row's run or the sentinel
         if (r > r0 && (rsu >> 10) == r - 1 && (rsu & 1023) <= q) k1_union<DBG>(P, k, ju);
         if (r + 1 < r1 && (rsd >> 10) == r + 1 && (rsd & 1023) <= q) k1_union<DBG>(P, jd, k);
+    };
+#if CCL_K1_STEAL
+    // the first T1 runs one per thread; beyond them (run-dense tiles) chunks
+    // of 32 runs from a shared counter, so warps whose unions finish early
+    // take more -- the phase ends at a barrier, i.e. at its slowest warp (on
+    // i.i.d. noise 44 % of K1's stall samples were barrier waits)
+    if (tid < total) run_unions(tid);
+    if (total > T1) {  // block-uniform
+#pragma unroll 1
+        for (;;) {
+            int k0 = 0;
+            if (lane == 0) k0 = atomicAdd(&sm.unext, 32);
+            k0 = __shfl_sync(kFull, k0, 0);
+            if (k0 >= total) break;
+            if (k0 + lane < total) run_unions(k0 + lane);
+        }
     }
+#else
+#pragma unroll 1
+    for (int k = tid; k < total; k += T1) run_unions(k);
+#endif
 #endif
     __syncthreads();
     if ((DBG & 4) && threadIdx.x == 0) k1_stamp(t, 3);
@@ -987,7 +1014,7 @@ __device__ __forceinline__ int k1_range(K1Smem<TY>& sm, const Geom& g, unsigned 
     const bool left = x0 > 0, right = x0 + kTileW < W;
     int32_t* Eh = E + size_t(t) * kEdgeCap;
 #pragma unroll 1
-    for (int k = tid; k < total; k += T1) {
+    for (int k = tid; k < total; k += T1) {  // (chunked work stealing here measured slower: 101.6 vs 100.7 us)
         const int root = find_r_ro(P, k);
         if (root != k) P[k] = root;  // an ancestor: concurrent finds stay valid
         const int rsk = rs[k];
