@@ -168,7 +168,10 @@ struct __align__(16) Word {
 // local root (row*1024 + x of its start); bits 16..31 = 1 + the root's index in
 // the tile's edge-root list if its component touches a tile edge (its final
 // label then comes from the boundary analysis), else 0.
-constexpr int kRunCache = 256;  // run records K3 prefetches per tile
+#ifndef CCL_K3_RUNCACHE
+#define CCL_K3_RUNCACHE 256
+#endif
+constexpr int kRunCache = CCL_K3_RUNCACHE;  // run records K3 prefetches per tile (128 per warp, warps 0..)
 constexpr int kRL = 32;         // run records of each boundary row K1 copies into the edge brief
 template <int TY>
 __host__ __device__ constexpr int runs_per_tile_cap() { return TY * kTileW / 2; }
@@ -1755,7 +1758,7 @@ struct __align__(1024) LinkSmem {
 template <int TY>
 struct LinkRegs {
     uint32_t m[TY / kWarps];
-    uint4 runs;  // warps 0, 2: run records 4*i .. 4*i+3 (i = lane, 32 + lane)
+    uint4 runs;  // warps w < kRunCache / 128: run records 4*i .. 4*i+3 (i = 32 * w + lane)
 };
 
 template <int TY>
@@ -1770,9 +1773,8 @@ __device__ __forceinline__ void k3_prefetch(const uint32_t* bits, const uint32_t
         const int y = id.y0 + warp + i * kWarps;
         pf.m[i] = (y < g.H && wg < g.WW) ? __ldg(bm + size_t(y) * g.WW + wg) : 0u;
     }
-    if (warp == 0 || warp == 2)
-        pf.runs = __ldg(reinterpret_cast<const uint4*>(R + size_t(t) * runs_per_tile_cap<TY>()) + lane +
-                        (warp == 2 ? 32 : 0));
+    if (warp < kRunCache / 128)
+        pf.runs = __ldg(reinterpret_cast<const uint4*>(R + size_t(t) * runs_per_tile_cap<TY>()) + lane + 32 * warp);
 }
 
 // TMA bulk-tensor store of one 1024-px label row from shared memory: the
@@ -1823,7 +1825,7 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
     const int tid = threadIdx.x;
     if ((DBG & 4) && threadIdx.x == 0) k3_stamp(t, 0);
 
-    if (warp == 0 || warp == 2) sm.rc[lane + (warp == 2 ? 32 : 0)] = cur.runs;
+    if (warp < kRunCache / 128) sm.rc[lane + 32 * warp] = cur.runs;
     if (tid == 0) {  // the helper warp has this tile's edge labels in slot j & 1
         while (ld_volatile(&sm.produced) <= j) __nanosleep(32);
     }
