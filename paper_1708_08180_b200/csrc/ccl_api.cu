@@ -356,7 +356,11 @@ cudaError_t run_stages(const Plan& p, int stages, const uint8_t* img, int32_t* o
 #define CCL_K2_SUB_MIN 0  // minimum split of a horizontal boundary: 2^SUB_MIN warps
 #endif
             int sub_log2 = CCL_K2_SUB_MIN;
-            while (sub_log2 < 2 && ((n_h << (sub_log2 + 1)) + n_v) <= (long long)sm_count() * 40) ++sub_log2;
+#ifndef CCL_K2_SUB_MAX
+#define CCL_K2_SUB_MAX 2
+#endif
+            while (sub_log2 < CCL_K2_SUB_MAX && ((n_h << (sub_log2 + 1)) + n_v) <= (long long)sm_count() * 40)
+                ++sub_log2;
 #ifndef CCL_K2_DBG
 #define CCL_K2_DBG 0  // timing experiments only (tools/build_variant.sh): 3 = skip K2, 4 = no unions
 #endif

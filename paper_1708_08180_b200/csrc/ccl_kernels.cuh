@@ -1711,7 +1711,10 @@ __device__ __forceinline__ int edge_label(const Geom& g, uint64_t* G, const Stri
 // The helper warp's shared slot holds the first kFlCap edge labels of a tile
 // (texture tiles use a few tens; only tiles labelled in several row ranges
 // exceed it -- the label table resolves those few entries itself).
-constexpr int kFlCap = 1088;
+#ifndef CCL_K3_FLCAP
+#define CCL_K3_FLCAP 1088
+#endif
+constexpr int kFlCap = CCL_K3_FLCAP;
 
 // ================================================================ K3: link
 // Final link (§2.3).  Per tile:
