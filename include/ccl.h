@@ -10,7 +10,8 @@
  *   (PAPER.md:24).  Input "Image I of size N x M" -- here H rows
  *   (the paper's M) by W columns (the paper's N = imgWidth), row-major, raster
  *   index idx(x,y) = y*W + x.  A pixel is foreground iff its
- *   byte is nonzero (reading R1).  Neighbourhood: 4-connectivity
+ *   byte is nonzero (reading R1; ccl_label_threshold_async: iff its
+ *   value >= a threshold).  Neighbourhood: 4-connectivity
  *    or 8-connectivity (north_star), clipped at the image border.
  *   Output label of pixel p: 0 if background, else 1 + the minimum raster index
  *   of p's component (the unique canonical form; reading R3).
