@@ -661,6 +661,9 @@ struct __align__(16) WordE {
 #ifndef CCL_K1_CAP16
 #define CCL_K1_CAP16 4576
 #endif
+#ifndef CCL_K1_DENSE_FROMBITS
+#define CCL_K1_DENSE_FROMBITS 0  // deferred run-dense tiles: masks read back from the bit mask
+#endif
 #ifndef CCL_K1_STEAL
 #define CCL_K1_STEAL 1  // union phase: runs beyond the first T1 in dynamic chunks of 32 per warp
 #endif
@@ -1193,8 +1196,11 @@ __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, cons
     // (32-row tiles: the warp's last two; INPLACE: all) are loaded first.
     constexpr int RPW = k1_rows_per_warp<TY>(), PFR = INPLACE ? 0 : k1_pf_rows<TY>();
     constexpr int NL = RPW - PFR > 0 ? RPW - PFR : 1;
+    // INPLACE (a deferred run-dense tile): its masks were written by the main
+    // loop's pass over it -- read them back from L2 instead of the image
+    constexpr bool FROMBITS = INPLACE && CCL_K1_DENSE_FROMBITS;
     uint4 lv[NL][2];
-    if (VEC) {
+    if (VEC && !FROMBITS) {
 #pragma unroll
         for (int i = PFR; i < RPW; ++i) {
             const int r = warp + i * k1_warps<TY>(), y = id.y0 + r, x = id.x0 + 32 * lane;
@@ -1208,7 +1214,10 @@ __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, cons
         if (r >= TY) break;  // warp-uniform
         const int y = id.y0 + r;
         uint32_t m = 0;
-        if (VEC) {
+        const int wg = id.tx * kWords + lane;
+        if (FROMBITS) {
+            m = (y < g.H && wg < g.WW) ? __ldcg(bm + size_t(y) * g.WW + wg) : 0u;
+        } else if (VEC) {
             // the lane's own 32 contiguous pixels: no cross-lane assembly
             const uint4 v0 = i < PFR ? cur.v[i < PFR ? i : 0][0] : lv[i >= PFR ? i - PFR : 0][0];
             const uint4 v1 = i < PFR ? cur.v[i < PFR ? i : 0][1] : lv[i >= PFR ? i - PFR : 0][1];
@@ -1223,8 +1232,7 @@ __device__ __forceinline__ int k1_masks(K1Smem<TY>& sm, const uint8_t* img, cons
                 if (lane == k) m = bal;
             }
         }
-        const int wg = id.tx * kWords + lane;
-        if (y < g.H && wg < g.WW) st_keep(bm + size_t(y) * g.WW + wg, m);
+        if (!FROMBITS && y < g.H && wg < g.WW) st_keep(bm + size_t(y) * g.WW + wg, m);
         k1_row_init<TY>(sm, r, lane, m);
     }
     // the pixels are in the masks now: the prefetch registers receive the
