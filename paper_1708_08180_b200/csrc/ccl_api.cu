@@ -239,10 +239,12 @@ bool encode_label_map(CUtensorMap* map, int32_t* out, const ccl::Geom& g) {
     if (!enc) return false;
     const cuuint64_t dims[3] = {32, cuuint64_t(g.W / 32), cuuint64_t(g.B) * cuuint64_t(g.H)};
     const cuuint64_t strides[2] = {128, cuuint64_t(g.W) * 4};
-    const cuuint32_t box[3] = {32, 32, 1};
+    // box: a whole row (32 words x 32 px, SWIZZLE_128B) or, CCL_K3_HALF, half of
+    // every word (32 words x 16 px, SWIZZLE_64B)
+    const cuuint32_t box[3] = {CCL_K3_HALF ? 16u : 32u, 32, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CCL_K3_HALF ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

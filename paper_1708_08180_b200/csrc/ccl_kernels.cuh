@@ -1756,9 +1756,10 @@ struct __align__(8) LWord {
 
 template <int TY>
 struct __align__(1024) LinkSmem {
-    // per-warp row of labels in the TMA SWIZZLE_128B layout: the 1024-px row is
-    // a 32 x 128 B box (one 128-B row per 32-px word); 16-B unit q of word w
-    // sits at w*128 + ((q ^ (w & 7)) * 16) -- also conflict-free for the lanes
+    // per-warp row of labels, two 2-KB halves in the TMA SWIZZLE_64B layout
+    // (CCL_K3_HALF; pixels 0-15 / 16-31 of every 32-px word, see tma_store_half),
+    // else one SWIZZLE_128B box (16-B unit q of word w at w*128 + ((q ^ (w & 7)) * 16));
+    // both conflict-free for the lanes
     int4 rowbuf[kWarps][kTileW / 4];
     LWord wd[TY][kWords];
     int32_t lab[kLabCap];            // final label of tile run k (current row window)
@@ -1804,6 +1805,23 @@ __device__ __forceinline__ void tma_store_row(const CUtensorMap* tmap, const voi
 }
 __device__ __forceinline__ void tma_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// CCL_K3_HALF: a row leaves as two half-row stores (pixels 0-15 / 16-31 of
+// every 32-px word: box [1][32][16], SWIZZLE_64B -- 16-B unit q of word w at
+// w*64 + ((q ^ ((w >> 1) & 3)) * 16)), so the wait for the previous row's
+// half to have been read overlaps the other half's expansion.
+#ifndef CCL_K3_HALF
+#define CCL_K3_HALF 1
+#endif
+__device__ __forceinline__ void tma_store_half(const CUtensorMap* tmap, const void* smem, int px0, int chunk0, int row) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(px0), "r"(chunk0), "r"(row), "r"(sa)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read_but1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -1914,8 +1932,11 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
             int32_t* orow = ob + size_t(y) * size_t(W) + x0;
             const int rb = sm.rbase[r] - base;
             if (VEC) {
-                if (TMA) {  // the previous row's bulk store must have read the buffer
-                    if (lane == 0) tma_wait_read_all();
+                if (TMA) {  // the previous row's bulk store (CCL_K3_HALF: its first half) must have read the buffer
+                    if (lane == 0) {
+                        if (CCL_K3_HALF) tma_wait_read_but1();
+                        else tma_wait_read_all();
+                    }
                     __syncwarp();
                 }
                 const LWord wd = sm.wd[r][lane];
@@ -1937,6 +1958,15 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
                 const uint32_t Lo = m & (~P1 | P2);   // code 1 (c) or 3 (L2)
 #pragma unroll
                 for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
+                    if (TMA && CCL_K3_HALF && q == 4) {  // first half out; the previous row's second half read
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_half(tmap, buf, 0, x0 >> 5, id.b * g.H + y);
+                            tma_wait_read_but1();
+                        }
+                        __syncwarp();
+                    }
                     const int L1 = sm.lab[min(idx + 1, lim)], L2 = sm.lab[min(idx + 2, lim)];
                     int px[4];
 #pragma unroll
@@ -1944,14 +1974,20 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
                         const uint32_t bit = 1u << (4 * q + j);
                         px[j] = selp_nz(Hi & bit, selp_nz(Lo & bit, L2, L1), selp_nz(Lo & bit, c, 0));
                     }
-                    buf[swz(lane, q)] = make_int4(px[0], px[1], px[2], px[3]);
+                    if (TMA && CCL_K3_HALF)
+                        buf[(q >> 2) * 128 + lane * 4 + ((q & 3) ^ ((lane >> 1) & 3))] = make_int4(px[0], px[1], px[2], px[3]);
+                    else
+                        buf[swz(lane, q)] = make_int4(px[0], px[1], px[2], px[3]);
                     c = px[3];  // pixel 3 background => the next fg pixel starts a run
                     idx += __popc((s >> (4 * q)) & 0xFu);
                 }
                 if (TMA) {
                     fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
                     __syncwarp();
-                    if (lane == 0) tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
+                    if (lane == 0) {
+                        if (CCL_K3_HALF) tma_store_half(tmap, buf + 128, 16, x0 >> 5, id.b * g.H + y);
+                        else tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
+                    }
                 } else {
                     __syncwarp();
 #pragma unroll 2
