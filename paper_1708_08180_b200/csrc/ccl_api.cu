@@ -239,13 +239,14 @@ bool encode_label_map(CUtensorMap* map, int32_t* out, const ccl::Geom& g) {
     if (!enc) return false;
     const cuuint64_t dims[3] = {32, cuuint64_t(g.W / 32), cuuint64_t(g.B) * cuuint64_t(g.H)};
     const cuuint64_t strides[2] = {128, cuuint64_t(g.W) * 4};
-    // box: a whole row (32 words x 32 px, SWIZZLE_128B) or, CCL_K3_HALF, half of
-    // every word (32 words x 16 px, SWIZZLE_64B)
-    const cuuint32_t box[3] = {CCL_K3_HALF ? 16u : 32u, 32, 1};
+    // box: a whole row (32 words x 32 px, SWIZZLE_128B) or, CCL_K3_SPLIT = 2 / 4,
+    // a half / quarter of every word (32 words x 16 / 8 px, SWIZZLE_64B / 32B)
+    const cuuint32_t box[3] = {cuuint32_t(32 / CCL_K3_SPLIT), 32, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    const CUtensorMapSwizzle sw = CCL_K3_SPLIT == 4 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : (CCL_K3_SPLIT == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CCL_K3_HALF ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Launch with programmatic stream serialisation (PDL): the kernel's blocks

@@ -1810,9 +1810,10 @@ __device__ __forceinline__ void tma_wait_read_all() {
 // every 32-px word: box [1][32][16], SWIZZLE_64B -- 16-B unit q of word w at
 // w*64 + ((q ^ ((w >> 1) & 3)) * 16)), so the wait for the previous row's
 // half to have been read overlaps the other half's expansion.
-#ifndef CCL_K3_HALF
-#define CCL_K3_HALF 1
+#ifndef CCL_K3_SPLIT
+#define CCL_K3_SPLIT 2  // stores per row: 1 (SWIZZLE_128B), 2 (64B) or 4 (32B)
 #endif
+#define CCL_K3_HALF (CCL_K3_SPLIT > 1)
 __device__ __forceinline__ void tma_store_half(const CUtensorMap* tmap, const void* smem, int px0, int chunk0, int row) {
     const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
@@ -1820,8 +1821,10 @@ __device__ __forceinline__ void tma_store_half(const CUtensorMap* tmap, const vo
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// all but the newest SPLIT - 1 bulk groups have read their shared memory
 __device__ __forceinline__ void tma_wait_read_but1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    if (CCL_K3_SPLIT == 4) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -1958,11 +1961,13 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
                 const uint32_t Lo = m & (~P1 | P2);   // code 1 (c) or 3 (L2)
 #pragma unroll
                 for (int q = 0; q < (DBG & 1 ? 0 : 8); ++q) {
-                    if (TMA && CCL_K3_HALF && q == 4) {  // first half out; the previous row's second half read
+                    constexpr int QP = 8 / CCL_K3_SPLIT;  // 4-px groups per part
+                    if (TMA && CCL_K3_HALF && q > 0 && q % QP == 0) {  // part out; the previous row's next part read
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_store_half(tmap, buf, 0, x0 >> 5, id.b * g.H + y);
+                            tma_store_half(tmap, buf + (q / QP - 1) * (256 / CCL_K3_SPLIT), (q / QP - 1) * (32 / CCL_K3_SPLIT),
+                                           x0 >> 5, id.b * g.H + y);
                             tma_wait_read_but1();
                         }
                         __syncwarp();
@@ -1974,8 +1979,10 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
                         const uint32_t bit = 1u << (4 * q + j);
                         px[j] = selp_nz(Hi & bit, selp_nz(Lo & bit, L2, L1), selp_nz(Lo & bit, c, 0));
                     }
-                    if (TMA && CCL_K3_HALF)
+                    if (TMA && CCL_K3_SPLIT == 2)
                         buf[(q >> 2) * 128 + lane * 4 + ((q & 3) ^ ((lane >> 1) & 3))] = make_int4(px[0], px[1], px[2], px[3]);
+                    else if (TMA && CCL_K3_SPLIT == 4)  // SWIZZLE_32B: unit u of word w at w*32 + ((u ^ ((w >> 2) & 1)) * 16)
+                        buf[(q >> 1) * 64 + lane * 2 + ((q & 1) ^ ((lane >> 2) & 1))] = make_int4(px[0], px[1], px[2], px[3]);
                     else
                         buf[swz(lane, q)] = make_int4(px[0], px[1], px[2], px[3]);
                     c = px[3];  // pixel 3 background => the next fg pixel starts a run
@@ -1985,7 +1992,9 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
                     fence_proxy_async_smem();  // generic-proxy smem writes -> async proxy
                     __syncwarp();
                     if (lane == 0) {
-                        if (CCL_K3_HALF) tma_store_half(tmap, buf + 128, 16, x0 >> 5, id.b * g.H + y);
+                        if (CCL_K3_HALF)
+                            tma_store_half(tmap, buf + (CCL_K3_SPLIT - 1) * (256 / CCL_K3_SPLIT),
+                                           (CCL_K3_SPLIT - 1) * (32 / CCL_K3_SPLIT), x0 >> 5, id.b * g.H + y);
                         else tma_store_row(tmap, buf, x0 >> 5, id.b * g.H + y);
                     }
                 } else {
