@@ -5,10 +5,7 @@ for v in ${TLDIR:-abvar}/tl_*.so; do
   cp $v paper_1708_08180_b200/libccl.so
   for k in ${KINDS:-texture}; do
     echo "== $(basename $v) $k" >> gpurun_out/timeline.txt
-    for d in ${DYNS:-1}; do
-      echo "-- CCL_K1_DYNAMIC=$d" >> gpurun_out/timeline.txt
-      CCL_K1_DYNAMIC=$d timeout 300 python tools/timeline.py $k >> gpurun_out/timeline.txt 2>&1
-    done
+    timeout 300 python tools/timeline.py $k >> gpurun_out/timeline.txt 2>&1
   done
 done
 cp /tmp/libccl.orig.so paper_1708_08180_b200/libccl.so
