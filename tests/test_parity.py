@@ -349,3 +349,18 @@ def test_strips_default_tile32(ccl, conn):
         for k in (1, 2):
             got = ccl.label_strips_emulated(t, k, conn).cpu().numpy()
             assert_same(got, want, f"strips {name} k={k} (32-row tiles)")
+
+
+@pytest.mark.parametrize("conn", CONNS)
+def test_tma_widths(ccl, conn):
+    """Widths that are multiples of 32 take K3's TMA half-row stores: rows
+    narrower than a tile and partial last tile columns are clipped by the
+    tensor map (W = 32 .. 2080), at every tile height."""
+    import torch
+    for W in (32, 64, 96, 992, 1056, 2080):
+        for H, seed in ((37, 1), (300, 2)):
+            img = synth.texture(H, W, seed=100 * W + seed, density=0.5)
+            want = oracle.label_bfs(img, conn)
+            t = torch.from_numpy(img).cuda()
+            for ty in (8, 16, 32):
+                assert_same(ccl.label(t, conn, tile_rows=ty).cpu().numpy(), want, f"{H}x{W} ty={ty}")
