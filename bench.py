@@ -431,6 +431,9 @@ def run_ours(args, rank, world, local):
     }
     if kern:
         line["kernels_ms"] = {k: round(v, 5) for k, v in kern.items()}
+        line["kernels_ms_note"] = ("each kernel timed as its own C-ABI stage call (L2 flushed): in the fused step K2 "
+                                   "runs under K1 and K3's inputs are L2-resident, so the sum exceeds ms_per_step; "
+                                   "fused-step timeline: profiles/r02_timeline.txt")
         dom = max(kern, key=kern.get)
         bpp = {"k1_local_merge": K1_BYTES_PER_PX, "k3_link": K3_BYTES_PER_PX}.get(dom)
         if bpp is not None:
