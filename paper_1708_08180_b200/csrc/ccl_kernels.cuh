@@ -661,6 +661,9 @@ struct __align__(16) WordE {
 #ifndef CCL_K1_CAP16
 #define CCL_K1_CAP16 4576
 #endif
+#ifndef CCL_K1_SCFENCE
+#define CCL_K1_SCFENCE 0  // a fence.sc before the ready flag (measured 0.3 us slower; the release suffices)
+#endif
 #ifndef CCL_K1_DENSE_FROMBITS
 #define CCL_K1_DENSE_FROMBITS 0  // deferred run-dense tiles: masks read back from the bit mask
 #endif
@@ -1273,7 +1276,12 @@ __device__ __forceinline__ void k1_publish(const Geom& g, unsigned t) {
     if (g.epoch) {  // every output of the tile is written
         __syncthreads();
         if (threadIdx.x == 0) {
+            // the barrier orders the block's writes before this thread's
+            // release, which is cumulative at gpu scope (st.release = a
+            // fence.acq_rel + the store); CCL_K1_SCFENCE adds a full fence.sc
+#if CCL_K1_SCFENCE
             __threadfence();
+#endif
             st_release_u64(g.ready + t, g.epoch);
             CCL_TL_MAX(7);
 #ifdef CCL_TIMELINE
