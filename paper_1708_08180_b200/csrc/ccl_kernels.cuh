@@ -1730,6 +1730,9 @@ __device__ __forceinline__ int edge_label(const Geom& g, uint64_t* G, const Stri
 // The helper warp's shared slot holds the first kFlCap edge labels of a tile
 // (texture tiles use a few tens; only tiles labelled in several row ranges
 // exceed it -- the label table resolves those few entries itself).
+#ifndef CCL_K3_TAILSYNC
+#define CCL_K3_TAILSYNC 0  // a barrier after each tile's last window as well (0.37 us/step slower)
+#endif
 #ifndef CCL_K3_TU
 #define CCL_K3_TU 4  // K3 label table: runs per thread and iteration (noise K3 137 -> 92 us; texture unchanged)
 #endif
@@ -2035,7 +2038,11 @@ __device__ __forceinline__ void k3_tile(LinkSmem<TY>& sm, const Geom& g, const u
             }
         }
         r0 = r1;
-        k3_sync();  // the table (and, after the last window, all smem) is reused
+        // the next window's table overwrites lab; after the tile's last window
+        // no barrier: each warp's next-tile writes (its own rows' words, the
+        // record cache) touch nothing another warp's expansion still reads, and
+        // the next tile's first barrier orders everything else
+        if (CCL_K3_TAILSYNC || r0 < TY) k3_sync();
     }
 #ifndef CCL_K3_DISCARD
 #define CCL_K3_DISCARD 1
